@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""PM+ hashing benchmark (BASELINE.json metric: "PM+ hashed GB/s (32/64-bit out)").
+
+Default workload = BASELINE.json configs[1] ("hashtable"): 2^24 strings with
+lengths U[8,64] bytes, packed contiguously with uint64 offsets, hashed with
+BOTH 64-bit and 32-bit PM+ (keys from seed 2).  One step = pmp_hash_batch with
+the PM+64 keys + pmp_hash_batch with the PM+32 keys over the resident batch.
+value = payload bytes hashed (both widths, all ranks) / max-over-ranks time.
+
+Multi-GPU (torchrun): each rank hashes its own batch of the same recipe
+(data seed 2 + 256*rank, same keys): weak scaling, no collective on the data
+path.  --workload long16g splits one 16 GiB string across ranks with one NCCL
+all-gather of 16-byte partials (strong scaling).
+
+--impl reference: the CPU oracle (oracle/, plain C) timed on a bounded sample
+of the same workload on the host cores (there is no other reference program:
+the paper ships no code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- workloads
+def make_batch(wl, rank, n=None):
+    """Host lengths/offsets for this rank's batch (data seed differs per rank)."""
+    n = wl.n if n is None else n
+    seed = wl.seed + 256 * rank
+    lens = datagen.lengths(wl.kind, seed, n, wl.lo, wl.hi)
+    offs = datagen.offsets_from_lengths(lens)
+    return seed, lens, offs
+
+
+def oracle_sample_rate(wl, seed, offs, bits_list, budget_s=12.0, max_threads=None):
+    """Oracle GB/s on a bounded prefix sample of the batch (all host threads)."""
+    import oracle
+
+    threads = max_threads or os.cpu_count() or 1
+    keys = {b: oracle.keygen(wl.seed, b) for b in bits_list}
+    # calibrate on 2^15 strings, then size the sample to ~budget_s
+    n_cal = min(1 << 15, offs.size - 1)
+    pay = datagen.payload_host(seed, 0, int(offs[n_cal]))
+    t0 = time.perf_counter()
+    for b in bits_list:
+        oracle.hash_batch(keys[b], pay, offs[:n_cal + 1], nthreads=threads)
+    dt = time.perf_counter() - t0
+    n_s = int(min(offs.size - 1, max(n_cal, n_cal * budget_s / max(dt, 1e-6))))
+    pay = datagen.payload_host(seed, 0, int(offs[n_s]))
+    t0 = time.perf_counter()
+    for b in bits_list:
+        oracle.hash_batch(keys[b], pay, offs[:n_s + 1], nthreads=threads)
+    dt = time.perf_counter() - t0
+    nbytes = int(offs[n_s]) * len(bits_list)
+    return nbytes / dt / 1e9, threads, f"first {n_s} strings of the batch ({int(offs[n_s])} B), widths {bits_list}", dt
+
+
+def oracle_long_rate(wl, nbytes_sample, budget_s=12.0):
+    import oracle
+
+    threads = os.cpu_count() or 1
+    k = oracle.keygen(wl.seed, 64)
+    pay = datagen.payload_host(wl.seed, 0, nbytes_sample)
+    t0 = time.perf_counter()
+    oracle.hash_long(k, pay, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return nbytes_sample / dt / 1e9, threads, f"first {nbytes_sample} B of the 16 GiB string hashed as one string", dt
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    unit = "GB/s"
+    times, rates = [], []
+    desc = cores = None
+    if wl.long:
+        for i in range(args.warmup + args.steps):
+            r, cores, desc, dt = oracle_long_rate(wl, 64 << 20)
+            if i >= args.warmup:
+                rates.append(r)
+                times.append(dt)
+    else:
+        seed, lens, offs = make_batch(wl, 0, n=min(wl.n, 1 << 22))
+        for i in range(args.warmup + args.steps):
+            r, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=4.0)
+            if i >= args.warmup:
+                rates.append(r)
+                times.append(dt)
+    v = statistics.median(rates)
+    line = {"impl": "reference", "metric": f"PM+ hashed GB/s ({'/'.join(str(b) for b in wl.bits)}-bit out)",
+            "value": v, "unit": unit, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * statistics.median(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64+u32" if len(wl.bits) > 1 else f"u{wl.bits[0]}",
+            "data": "synthetic (seeded xoshiro256** bytes)", "config": workload_config(wl, args.gpus),
+            "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(wl, gpus):
+    c = {"workload": wl.name, "strings_per_gpu": wl.n, "len_bytes": [wl.lo, wl.hi],
+         "len_dist": {0: "fixed", 1: "uniform", 2: "log-uniform"}[wl.kind], "bits": list(wl.bits),
+         "key_seed": wl.seed, "parallelism": f"dp{gpus}" if not wl.long else f"split{gpus}",
+         "l2": "inputs larger than L2 (126 MB); no flush needed"}
+    if wl.long:
+        c["strings_per_gpu"] = None
+        c["string_bytes"] = wl.lo
+    return c
+
+
+# ----------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="pmp", choices=["pmp", "reference"])
+    ap.add_argument("--workload", default="hashtable", choices=sorted(datagen.WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = datagen.WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_09840_b200 as pmp
+    from paper_1609_09840_b200 import _build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if _build.needs_build() and rank == 0:
+        _build.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    sp = int(stream.cuda_stream)
+
+    keys = {b: pmp.Keys.generate(wl.seed, b) for b in wl.bits}
+    outs = {}
+    if wl.long:
+        total = wl.lo
+        begins = pmp.pmp_long_split(64, total, world)
+        lo, hi = begins[rank], begins[rank + 1]
+        d_data = torch.empty(hi - lo + 16, dtype=torch.uint8, device=dev)
+        # rank's slice of the string: regenerate its pages (page-aligned since lo % 4096 == 0)
+        assert lo % datagen.PAGE == 0
+        d_full = d_data[: hi - lo]
+        fill_slice(wl.seed, d_full, lo, sp)
+        parts = torch.zeros(2 * world, dtype=torch.int64, device=dev)
+        out = torch.zeros(1, dtype=torch.int64, device=dev)
+        payload_bytes = total
+
+        def step():
+            pmp._check(pmp.pmp_hash_long_partial(keys[64].handle, d_full.data_ptr(), hi - lo, lo, total,
+                                                 parts[2 * rank:2 * rank + 2].data_ptr(), sp), "partial")
+            if world > 1:
+                dist.all_gather_into_tensor(parts, parts[2 * rank:2 * rank + 2].clone())
+            pmp._check(pmp.pmp_hash_long_combine(keys[64].handle, parts.data_ptr(), world, total,
+                                                 out.data_ptr(), sp), "combine")
+        dominant = "k_node"
+        alg_bytes_per_launch = hi - lo
+        n = 1
+    else:
+        seed, lens, offs = make_batch(wl, rank)
+        n = wl.n
+        total_bytes = int(offs[-1])
+        d_pay = torch.empty(total_bytes + 16, dtype=torch.uint8, device=dev)
+        datagen.fill_device(seed, d_pay.data_ptr(), total_bytes, sp)
+        d_off = torch.from_numpy(offs.view(np.int64)).to(dev)
+        for b in wl.bits:
+            outs[b] = torch.empty(n, dtype=torch.int64 if b == 64 else torch.int32, device=dev)
+        payload_bytes = total_bytes * len(wl.bits)
+
+        def step():
+            for b in wl.bits:
+                pmp._check(pmp.pmp_hash_batch(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
+                                              outs[b].data_ptr(), sp), "pmp_hash_batch")
+        dominant = "k_short" if wl.hi <= 127 else "k_wstring"
+        # algorithmic bytes per dominant launch: payload + offsets + digests (avg over widths)
+        alg_bytes_per_launch = total_bytes + 8 * (n + 1) + n * sum(b // 8 for b in wl.bits) / len(wl.bits)
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = pmp.pmp_launch_count()
+    pmp.pmp_prof_reset()
+    pmp.pmp_prof_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    pmp.pmp_prof_enable(False)
+    launches = pmp.pmp_launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    k_ms, k_cnt = pmp.pmp_prof_read(dominant)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    if wl.long:
+        value = payload_bytes / (ms_per_step / 1000) / 1e9
+    else:
+        value = payload_bytes * world / (ms_per_step / 1000) / 1e9
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, wl, pmp, keys, dev, stream, rank, world)
+
+    line = None
+    if rank == 0:
+        peak, peak_src = hbm_peak()
+        avg_ms = k_ms / max(k_cnt, 1)
+        achieved = alg_bytes_per_launch / (avg_ms / 1000) / 1e9 if k_cnt else None
+        traffic = load_traffic(wl.name, dominant)
+        clocks = clk.summary()
+        cpu = None
+        if not args.no_cpu:
+            cpu = cpu_baseline(wl)
+        line = {
+            "metric": f"PM+ hashed GB/s ({'/'.join(str(b) for b in wl.bits)}-bit out)",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if wl.long else "weak", "vs_baseline": None,
+            "dtype": "u64+u32" if len(wl.bits) > 1 else f"u{wl.bits[0]}",
+            "data": "synthetic (seeded xoshiro256** bytes, generated on device)",
+            "config": workload_config(wl, world),
+            "bytes_per_gpu_cycle": (value / world * 1e9) / (clocks["sm_mhz"] * 1e6) if clocks.get("sm_mhz") else None,
+            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "alg_bytes_per_launch": alg_bytes_per_launch, "avg_launch_ms": avg_ms,
+                         "launches_timed": k_cnt},
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def fill_slice(seed, d_buf, start, sp):
+    """Regenerate payload bytes [start, start + len) of the stream on device."""
+    datagen.fill_device(seed, d_buf.data_ptr(), d_buf.numel(), sp, start=start)
+
+
+def run_e2e(args, wl, pmp, keys, dev, stream, rank, world):
+    import torch
+
+    if wl.long:
+        return None
+    seed, lens, offs = make_batch(wl, rank)
+    n = wl.n
+    total = int(offs[-1])
+    h_pay = torch.from_numpy(datagen.payload_host(seed, 0, total)).pin_memory()
+    h_off = torch.from_numpy(offs.view(np.int64)).pin_memory()
+    d_pay = torch.empty(total + 16, dtype=torch.uint8, device=dev)
+    d_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    d_out = {b: torch.empty(n, dtype=torch.int64 if b == 64 else torch.int32, device=dev) for b in wl.bits}
+    h_out = {b: torch.empty(n, dtype=d_out[b].dtype).pin_memory() for b in wl.bits}
+    sp = int(stream.cuda_stream)
+
+    def step():
+        d_pay[:total].copy_(h_pay, non_blocking=True)
+        d_off.copy_(h_off, non_blocking=True)
+        for b in wl.bits:
+            pmp._check(pmp.pmp_hash_batch(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
+                                          d_out[b].data_ptr(), sp), "e2e hash")
+            h_out[b].copy_(d_out[b], non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.e2e_steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.e2e_steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": total * len(wl.bits) * world / (ms / 1000) / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": total + 8 * (n + 1),
+            "d2h_bytes_per_step": n * sum(b // 8 for b in wl.bits), "ms_per_step": ms,
+            "path": "pinned host -> cudaMemcpyAsync -> pmp_hash_batch (both widths) -> host"}
+
+
+def cpu_baseline(wl):
+    try:
+        if wl.long:
+            v, cores, desc, dt = oracle_long_rate(wl, 256 << 20)
+        else:
+            seed, lens, offs = make_batch(wl, 0, n=min(wl.n, 1 << 23))
+            v, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=10.0)
+        return {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc,
+                "seconds": dt}
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "GB/s", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
+
+
+def load_traffic(workload, kernel):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,150 @@
+/*
+ * pmp.h -- C ABI of libpmp.so: PM+ hashing (Ivanchykhin, Ignatchenko, Lemire,
+ * "Regular and almost universal hashing: an efficient implementation",
+ * arXiv:1609.09840) on NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" is line n of the paper's LaTeX source; "S:n" is
+ * line n of SPEC.md.  Ambiguous passages follow the readings Q1..Q16 listed in
+ * DESIGN.md ("Readings of the paper").
+ *
+ * What is computed: for a byte string s,
+ *   sigma  = s || 0x01 || 0x00...  up to a multiple of w = n/8 bytes, read as
+ *            little-endian n-bit words (readings Q3, Q4);
+ *   V      = Tree(sigma): Algorithm 1 with the PM+-Multilinear
+ *            family f_j(x_1..x_128) = (b_j + sum_i a_{j,i} x_i) mod p, Eq. (1)
+ *            P:543, f_1 at the leaves (reading Q1); when sigma has one word the
+ *            loop never runs and V = sigma_0 (reading Q2);
+ *   digest = mix_n(V mod 2^n) with the finaliser of P:722-734.
+ * PM+64: n = 64, p = 2^64+13; PM+32: n = 32, p = 2^32+15 (Table 2).
+ *
+ * Conventions for every call:
+ *   - Return 0 on success or a negative PMP_E* code (pmp_strerror()).
+ *   - Pointers marked (device) are device memory of the key handle's device,
+ *     owned by the caller; the library writes only the `out` / `partial`
+ *     buffers and allocates its scratch stream-ordered (cudaMallocAsync).
+ *   - Hash calls are asynchronous and ordered on `stream` (a cudaStream_t; NULL
+ *     is the legacy default stream).  Results are valid after the stream is
+ *     synchronised; execution faults surface there, launch errors are returned
+ *     as PMP_ECUDA.
+ *   - No CPU fallback exists: without a CUDA device every hash call returns
+ *     PMP_ENODEV.
+ */
+#ifndef PMP_H
+#define PMP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+struct CUstream_st; /* = cudaStream_t */
+
+#define PMP_OK 0
+#define PMP_EINVAL (-1)   /* bad argument (NULL with n > 0, bad width, key out of range, misaligned split) */
+#define PMP_ETOOLONG (-2) /* more than 2^56 - 1 words (Table 3: L = 8 levels of m = 128) */
+#define PMP_ECUDA (-3)    /* CUDA runtime error at launch / allocation */
+#define PMP_ENOMEM (-4)   /* host or device allocation failure */
+#define PMP_ENODEV (-5)   /* no CUDA device, or the key handle has no device copy */
+
+/* Opaque key schedule: b_j and a_{j,1..128} for j = 1..8 (Alg. 1 REQUIRE,
+ * P:431; Eq. (1)).  Immutable after creation; may be shared by any
+ * number of threads and streams on its device. */
+typedef struct pmp_keys pmp_keys;
+
+/* Expand `seed` into a key schedule for out_bits = 32 or 64 and upload it to
+ * the current CUDA device.  Key-generation contract (reading Q12; the paper is
+ * silent): xoshiro256** seeded with 4 splitmix64 outputs of `seed`; per level
+ * j = 1..8, b_j = x (x>>32 for 32-bit) then a_{j,i} by rejection sampling to
+ * [1, p - kappa - 1] (kappa = 24 / 28).  Every process calling
+ * with the same seed gets identical keys.  Returns NULL on a bad width or
+ * allocation failure.  Without a CUDA device the handle is created host-only
+ * (export works, hash calls return PMP_ENODEV). */
+pmp_keys *pmp_keygen(uint64_t seed, int out_bits);
+
+/* Build a schedule from explicit words (host arrays: b[8], a[8*128],
+ * level-major).  Validates b_j < 2^n and 1 <= a_{j,i} <= p - kappa - 1
+ * (SPEC "KeyOutOfRange"); returns NULL when a key is out of range. */
+pmp_keys *pmp_keys_from_words(int out_bits, const uint64_t *b, const uint64_t *a);
+
+/* Copy the schedule to host arrays b[8], a[8*128]; returns 0 or PMP_EINVAL. */
+int pmp_keys_export(const pmp_keys *keys, uint64_t *b, uint64_t *a);
+
+/* 32 or 64, or PMP_EINVAL for NULL. */
+int pmp_keys_bits(const pmp_keys *keys);
+
+void pmp_keys_free(pmp_keys *keys);
+
+/* Hash n byte strings.  String i is bytes[offsets[i], offsets[i+1]) (CSR,
+ * reading Q13); strings may start at any byte alignment and may be empty.
+ *   bytes   (device) payload; only bytes inside [offsets[0], offsets[n]) are
+ *           used -- the kernels read whole aligned 16-byte units that contain
+ *           at least one such byte, never a unit outside that range;
+ *   offsets (device) n+1 uint64, non-decreasing (precondition, not checked);
+ *   out     (device) n digests: uint64 for 64-bit keys, uint32 for 32-bit keys,
+ *           in string order.
+ * n == 0 is a no-op; n must be < 2^32.  Strings of <= 127 bytes take the
+ * thread-per-string path, longer ones a warp per string. */
+int pmp_hash_batch(const pmp_keys *keys, const uint8_t *bytes, const uint64_t *offsets,
+                   uint64_t n, void *out, struct CUstream_st *stream);
+
+/* Hash one string of `len` bytes at `bytes` (device, any alignment); writes
+ * one digest (uint64 / uint32) to `out` (device).  Block-parallel over the
+ * level-2 nodes of the tree (128 level-1 blocks each), then one launch per
+ * upper level.  PMP_ETOOLONG beyond 2^56 - 1 words. */
+int pmp_hash_long(const pmp_keys *keys, const uint8_t *bytes, uint64_t len, void *out,
+                  struct CUstream_st *stream);
+
+/* Multi-GPU split of one long string (the tree is affine in its level-1 block
+ * values):
+ * The caller holds bytes [global_offset, global_offset + local_len) of a string
+ * of total_len bytes at `local` (device).  global_offset must be a multiple of
+ * the level-1 block size (1024 bytes for PM+64, 512 for PM+32) and so must
+ * local_len unless global_offset + local_len == total_len (the caller owning the
+ * tail, which also owns the marker word).  Writes to `partial` (device, 2
+ * uint64: lo, hi) the field element P = sum over the caller's blocks c of
+ * K_c * v_1(c) mod p, where K_c is the product of the level keys on c's path
+ * to the root.  Ranges of all callers must tile [0, total_len). */
+int pmp_hash_long_partial(const pmp_keys *keys, const uint8_t *local, uint64_t local_len,
+                          uint64_t global_offset, uint64_t total_len, uint64_t *partial,
+                          struct CUstream_st *stream);
+
+/* Combine G partials (device, 2*G uint64, e.g. the result of an all-gather):
+ * V = C(total_len) + sum_g P_g mod p, C being the key-only tree value with
+ * all v_1 = 0; writes the digest to `out` (device). */
+int pmp_hash_long_combine(const pmp_keys *keys, const uint64_t *partials, int G,
+                          uint64_t total_len, void *out, struct CUstream_st *stream);
+
+/* Host-only helper: split [0, total_len) into G contiguous ranges aligned to
+ * level-1 blocks with equal block counts (+- 1); begins[0..G] (host),
+ * begins[G] = total_len.  Returns 0 or PMP_EINVAL. */
+int pmp_long_split(int out_bits, uint64_t total_len, int G, uint64_t *begins);
+
+/* Host-only helper (test hook): the key-only constant C(total_len) as (lo, hi). */
+int pmp_long_constant(const pmp_keys *keys, uint64_t total_len, uint64_t *c2);
+
+/* Device self-test hooks running the hot path's own device functions:
+ * mode 0: in = n triples (w0, w1, w2) -> (w0 + w1 2^n + w2 2^2n) mod p via the
+ *         Section 6.2 reduction and Algorithm 2; w2 <= 2^16;
+ * mode 1: in = n records [b, a_0..a_127, s_0..s_127] -> Eq. (1) via the
+ *         hot-loop multiply-accumulate;
+ * mode 2: in = n words -> mix_n(word).
+ * in/out (device); out gets 2 uint64 per record (lo, hi). */
+int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_t *out,
+                 struct CUstream_st *stream);
+
+/* Instrumentation.  pmp_launch_count(): kernels launched by this library so
+ * far in this process.  With pmp_prof_enable(1), every launch is bracketed
+ * by CUDA events on its own stream; pmp_prof_read() synchronises those events
+ * and returns the summed milliseconds and launch count of kernels whose name
+ * starts with `prefix` ("k_short", "k_wstring", "k_node", ...). */
+uint64_t pmp_launch_count(void);
+void pmp_prof_enable(int on);
+void pmp_prof_reset(void);
+int pmp_prof_read(const char *prefix, double *ms, uint64_t *count);
+
+const char *pmp_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,244 @@
+"""PM+ hashing on B200 -- thin Python binding over libpmp.so (include/pmp.h).
+
+Argument marshalling only: every step of the hash runs in the CUDA kernels of
+``csrc/``.  The functions keep the C names (``pmp_keygen``, ``pmp_hash_batch``,
+``pmp_hash_long``, ...) and take raw integers for device pointers and streams;
+the ``hash_batch`` / ``hash_long`` conveniences accept torch CUDA tensors and
+use torch only for device memory and the current stream.
+
+There is no CPU fallback: importing works without a GPU (for the ABI checks),
+but every hash call fails loudly when no CUDA device is present.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import _build
+
+LIB_PATH = _build.LIB
+
+PMP_OK, PMP_EINVAL, PMP_ETOOLONG, PMP_ECUDA, PMP_ENOMEM, PMP_ENODEV = 0, -1, -2, -3, -4, -5
+
+_u64, _vp, _int = ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int
+_lib = None
+
+
+class PmpError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {strerror(code)} ({code})")
+        self.code = code
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree libpmp.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build()")
+        h = ctypes.CDLL(LIB_PATH)
+        sig = {
+            "pmp_keygen": ([_u64, _int], _vp),
+            "pmp_keys_from_words": ([_int, _vp, _vp], _vp),
+            "pmp_keys_export": ([_vp, _vp, _vp], _int),
+            "pmp_keys_bits": ([_vp], _int),
+            "pmp_keys_free": ([_vp], None),
+            "pmp_hash_batch": ([_vp, _vp, _vp, _u64, _vp, _vp], _int),
+            "pmp_hash_long": ([_vp, _vp, _u64, _vp, _vp], _int),
+            "pmp_hash_long_partial": ([_vp, _vp, _u64, _u64, _u64, _vp, _vp], _int),
+            "pmp_hash_long_combine": ([_vp, _vp, _int, _u64, _vp, _vp], _int),
+            "pmp_long_split": ([_int, _u64, _int, _vp], _int),
+            "pmp_long_constant": ([_vp, _u64, _vp], _int),
+            "pmp_selftest": ([_int, _int, _vp, _u64, _vp, _vp], _int),
+            "pmp_launch_count": ([], _u64),
+            "pmp_prof_enable": ([_int], None),
+            "pmp_prof_reset": ([], None),
+            "pmp_prof_read": ([ctypes.c_char_p, _vp, _vp], _int),
+            "pmp_strerror": ([_int], ctypes.c_char_p),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(h, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = h
+    return _lib
+
+
+def strerror(code: int) -> str:
+    return lib().pmp_strerror(code).decode()
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise PmpError(rc, what)
+
+
+# --------------------------------------------------------------- C-named calls
+def pmp_keygen(seed: int, out_bits: int) -> int:
+    return lib().pmp_keygen(seed & (2**64 - 1), out_bits) or 0
+
+
+def pmp_keys_from_words(out_bits: int, b_ptr: int, a_ptr: int) -> int:
+    return lib().pmp_keys_from_words(out_bits, b_ptr, a_ptr) or 0
+
+
+def pmp_keys_export(keys: int, b_ptr: int, a_ptr: int) -> int:
+    return lib().pmp_keys_export(keys, b_ptr, a_ptr)
+
+
+def pmp_keys_free(keys: int) -> None:
+    lib().pmp_keys_free(keys)
+
+
+def pmp_hash_batch(keys: int, bytes_ptr: int, offsets_ptr: int, n: int, out_ptr: int, stream: int) -> int:
+    return lib().pmp_hash_batch(keys, bytes_ptr, offsets_ptr, n, out_ptr, stream)
+
+
+def pmp_hash_long(keys: int, bytes_ptr: int, length: int, out_ptr: int, stream: int) -> int:
+    return lib().pmp_hash_long(keys, bytes_ptr, length, out_ptr, stream)
+
+
+def pmp_hash_long_partial(keys: int, local_ptr: int, local_len: int, global_offset: int,
+                          total_len: int, partial_ptr: int, stream: int) -> int:
+    return lib().pmp_hash_long_partial(keys, local_ptr, local_len, global_offset, total_len,
+                                       partial_ptr, stream)
+
+
+def pmp_hash_long_combine(keys: int, partials_ptr: int, G: int, total_len: int, out_ptr: int,
+                          stream: int) -> int:
+    return lib().pmp_hash_long_combine(keys, partials_ptr, G, total_len, out_ptr, stream)
+
+
+def pmp_selftest(out_bits: int, mode: int, in_ptr: int, n: int, out_ptr: int, stream: int) -> int:
+    return lib().pmp_selftest(out_bits, mode, in_ptr, n, out_ptr, stream)
+
+
+def pmp_launch_count() -> int:
+    return int(lib().pmp_launch_count())
+
+
+def pmp_prof_enable(on: bool) -> None:
+    lib().pmp_prof_enable(1 if on else 0)
+
+
+def pmp_prof_reset() -> None:
+    lib().pmp_prof_reset()
+
+
+def pmp_prof_read(prefix: str) -> tuple[float, int]:
+    ms = ctypes.c_double()
+    cnt = ctypes.c_uint64()
+    _check(lib().pmp_prof_read(prefix.encode(), ctypes.byref(ms), ctypes.byref(cnt)), "pmp_prof_read")
+    return ms.value, cnt.value
+
+
+def pmp_long_split(out_bits: int, total_len: int, G: int) -> list[int]:
+    arr = (ctypes.c_uint64 * (G + 1))()
+    _check(lib().pmp_long_split(out_bits, total_len, G, arr), "pmp_long_split")
+    return [int(x) for x in arr]
+
+
+# --------------------------------------------------------------- conveniences
+class Keys:
+    """Owning wrapper of a ``pmp_keys*`` handle (device copy on the current device)."""
+
+    def __init__(self, handle: int, bits: int):
+        if not handle:
+            raise PmpError(PMP_EINVAL, "pmp_keygen / pmp_keys_from_words returned NULL")
+        self.handle = handle
+        self.bits = bits
+
+    @classmethod
+    def generate(cls, seed: int, bits: int) -> "Keys":
+        return cls(pmp_keygen(seed, bits), bits)
+
+    @classmethod
+    def from_words(cls, bits: int, b, a) -> "Keys":
+        import numpy as np
+
+        b = np.ascontiguousarray(b, dtype=np.uint64)
+        a = np.ascontiguousarray(a, dtype=np.uint64).reshape(-1)
+        assert b.size == 8 and a.size == 8 * 128
+        return cls(pmp_keys_from_words(bits, b.ctypes.data, a.ctypes.data), bits)
+
+    def export(self):
+        import numpy as np
+
+        b = np.zeros(8, dtype=np.uint64)
+        a = np.zeros(8 * 128, dtype=np.uint64)
+        _check(pmp_keys_export(self.handle, b.ctypes.data, a.ctypes.data), "pmp_keys_export")
+        return b, a.reshape(8, 128)
+
+    def close(self) -> None:
+        if self.handle:
+            pmp_keys_free(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def hash_batch(keys: Keys, payload, offsets, out=None, stream=None):
+    """Hash the CSR batch (``payload`` uint8 CUDA tensor, ``offsets`` int64/uint64
+    CUDA tensor of n+1 entries).  Returns ``out`` (uint64 or uint32 view in an
+    int64/int32 tensor) -- asynchronous on the current torch stream."""
+    import torch
+
+    n = offsets.numel() - 1
+    if out is None:
+        out = torch.empty(max(n, 0), dtype=torch.int64 if keys.bits == 64 else torch.int32,
+                          device=offsets.device)
+    _check(pmp_hash_batch(keys.handle, payload.data_ptr(), offsets.data_ptr(), max(n, 0),
+                          out.data_ptr(), _stream_ptr(stream)), "pmp_hash_batch")
+    return out
+
+
+def hash_long(keys: Keys, data, length: int | None = None, out=None, stream=None):
+    import torch
+
+    length = data.numel() if length is None else length
+    if out is None:
+        out = torch.empty(1, dtype=torch.int64 if keys.bits == 64 else torch.int32, device=data.device)
+    _check(pmp_hash_long(keys.handle, data.data_ptr(), length, out.data_ptr(), _stream_ptr(stream)),
+           "pmp_hash_long")
+    return out
+
+
+def hash_long_partial(keys: Keys, local, local_len: int, global_offset: int, total_len: int,
+                      partial=None, stream=None):
+    import torch
+
+    if partial is None:
+        partial = torch.zeros(2, dtype=torch.int64, device=local.device)
+    _check(pmp_hash_long_partial(keys.handle, local.data_ptr(), local_len, global_offset, total_len,
+                                 partial.data_ptr(), _stream_ptr(stream)), "pmp_hash_long_partial")
+    return partial
+
+
+def hash_long_combine(keys: Keys, partials, total_len: int, out=None, stream=None):
+    import torch
+
+    G = partials.numel() // 2
+    if out is None:
+        out = torch.empty(1, dtype=torch.int64 if keys.bits == 64 else torch.int32, device=partials.device)
+    _check(pmp_hash_long_combine(keys.handle, partials.data_ptr(), G, total_len, out.data_ptr(),
+                                 _stream_ptr(stream)), "pmp_hash_long_combine")
+    return out
+
+
+def as_u64(t) -> "object":
+    """Digest tensor (int64/int32) -> numpy uint64/uint32 on host."""
+    import numpy as np
+
+    a = t.detach().cpu().numpy()
+    return a.view(np.uint64) if a.dtype == np.int64 else a.view(np.uint32)

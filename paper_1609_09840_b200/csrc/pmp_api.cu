@@ -1,0 +1,485 @@
+// pmp_api.cu -- libpmp.so: the C ABI declared in include/pmp.h.
+//
+// Host side of the PM+ path: key generation (project contract, reading Q12),
+// argument checks, tree geometry, the key-only constant of the affine split,
+// stream-ordered scratch, kernel launches and launch instrumentation.  Every
+// step of the hash itself runs in the kernels of pmp_kernels.cuh; there is no
+// CPU fallback.
+#include "../../include/pmp.h"
+#include "pmp_kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace pmp;
+
+struct pmp_keys {
+  int bits;
+  uint64_t b[kL];
+  uint64_t a[kL * kM];
+  int device;       // -1: host-only handle
+  uint64_t *d_blob; // device: b[8] then a[8*128]
+};
+
+namespace {
+
+typedef unsigned __int128 u128;
+
+// ----------------------------------------------------------------- keygen
+uint64_t splitmix(uint64_t &s) {
+  uint64_t z = (s += 0x9E3779B97F4A7C15ULL);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+struct Xoshiro {
+  uint64_t s[4];
+  static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+  uint64_t next() {
+    const uint64_t result = rotl(s[1] * 5, 7) * 9;
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return result;
+  }
+};
+
+uint64_t amax_of(int bits) {  // p - kappa - 1
+  return bits == 64 ? 0xFFFFFFFFFFFFFFF4ULL /* 2^64 - 12 */ : 0xFFFFFFF2ULL /* 2^32 - 14 */;
+}
+u128 prime_of(int bits) { return bits == 64 ? (((u128)1 << 64) + 13) : (((u128)1 << 32) + 15); }
+
+int upload(pmp_keys *k) {
+  k->device = -1;
+  k->d_blob = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return 0;  // host-only handle
+  }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return PMP_ECUDA;
+  std::vector<uint64_t> blob(kL + kL * kM);
+  memcpy(blob.data(), k->b, sizeof(k->b));
+  memcpy(blob.data() + kL, k->a, sizeof(k->a));
+  if (cudaMalloc(&k->d_blob, blob.size() * 8) != cudaSuccess) return PMP_ENOMEM;
+  if (cudaMemcpy(k->d_blob, blob.data(), blob.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(k->d_blob);
+    k->d_blob = nullptr;
+    return PMP_ECUDA;
+  }
+  k->device = dev;
+  return 0;
+}
+
+// ----------------------------------------------------------------- device info
+struct DevInfo {
+  int sms = 0;
+  bool init = false;
+};
+std::mutex g_mu;
+DevInfo g_dev[64];
+
+int sm_count(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!g_dev[dev].init) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_dev[dev].sms = v > 0 ? v : 148;
+    g_dev[dev].init = true;
+  }
+  return g_dev[dev].sms;
+}
+
+// ----------------------------------------------------------------- instrumentation
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_prof{0};
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+std::vector<ProfRec> g_pending;
+std::vector<std::pair<std::string, std::pair<double, uint64_t>>> g_done;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t get_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <class F>
+int launch(const char *name, cudaStream_t st, F &&f) {
+  const bool prof = g_prof.load(std::memory_order_relaxed) != 0;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (prof) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    a = get_event();
+    b = get_event();
+  }
+  if (prof) cudaEventRecord(a, st);
+  f();
+  cudaError_t e = cudaGetLastError();
+  if (prof) {
+    cudaEventRecord(b, st);
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_pending.push_back({name, a, b});
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return e == cudaSuccess ? 0 : PMP_ECUDA;
+}
+
+int check_keys(const pmp_keys *k) {
+  if (!k) return PMP_EINVAL;
+  if (!k->d_blob) return PMP_ENODEV;
+  return 0;
+}
+
+ParamKeys param_keys(const pmp_keys *k) {
+  ParamKeys pk;
+  for (int i = 0; i < 32; i++) pk.a[i] = k->a[i];
+  pk.b = k->b[0];
+  return pk;
+}
+
+// ----------------------------------------------------------------- geometry
+int chunk_bytes(int bits) { return bits == 64 ? 1024 : 512; }
+uint64_t words_of(int bits, uint64_t len) { return len / (uint64_t)(bits / 8) + 1; }
+
+// C = root value of the tree whose level-1 values are all 0.  At
+// level j >= 2 every node except the last of its level has 128 children that
+// are themselves non-last nodes, so two values per level suffice.
+u128 long_constant(const pmp_keys *k, uint64_t len) {
+  const Geom gm = make_geom(words_of(k->bits, len));
+  if (gm.leff <= 1) return 0;
+  const u128 p = prime_of(k->bits);
+  u128 cf = 0, cl = 0;  // level 1: all zero
+  for (int j = 2; j <= gm.leff; j++) {
+    const uint64_t *aj = k->a + (uint64_t)(j - 1) * kM;
+    const uint64_t nprev = gm.T[j - 1], ncur = gm.T[j];
+    const uint64_t last_children = nprev - 128 * (ncur - 1);
+    u128 nf = k->b[j - 1] % p, nl = k->b[j - 1] % p;
+    for (uint64_t r = 0; r < 128; r++) nf = (nf + ((u128)aj[r] * cf) % p) % p;
+    for (uint64_t r = 0; r + 1 < last_children; r++) nl = (nl + ((u128)aj[r] * cf) % p) % p;
+    nl = (nl + ((u128)aj[last_children - 1] * cl) % p) % p;
+    cf = nf;
+    cl = nl;
+  }
+  return cl;
+}
+
+const char *kErr[] = {"ok", "invalid argument", "string too long (> 2^56-1 words)", "CUDA error",
+                      "out of memory", "no CUDA device for this key handle"};
+
+struct Scratch {
+  void *p = nullptr;
+  cudaStream_t st;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  int alloc(size_t n) { return cudaMallocAsync(&p, n, st) == cudaSuccess ? 0 : PMP_ENOMEM; }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+template <int BITS>
+int long_partial_impl(const pmp_keys *k, const uint8_t *local, uint64_t local_len, uint64_t g0,
+                      uint64_t total, uint64_t *partial, cudaStream_t st) {
+  const uint64_t CB = (uint64_t)chunk_bytes(BITS);
+  const Geom gm = make_geom(words_of(BITS, total));
+  StrView s;
+  s.base = local;
+  s.g0 = g0;
+  s.avail_end = g0 + local_len;
+  s.B = total;
+  s.delta = (uint32_t)((uintptr_t)local & 15);
+  const bool owns_tail = g0 + local_len == total;
+  const uint64_t cb = g0 / CB;
+  const uint64_t ce = owns_tail ? gm.T[1] : (g0 + local_len) / CB;
+  const int sms = sm_count(k->device);
+  if (gm.leff <= 1) {  // one level-1 block (or none): only the caller holding byte 0 contributes
+    if (cb == 0 && ce >= 1) {
+      return launch("k_node", st, [&] { k_node<BITS><<<1, kWWarps * 32, 0, st>>>(k->d_blob, s, 0, 1, 0, 1, 1, partial); });
+    }
+    return cudaMemsetAsync(partial, 0, 16, st) == cudaSuccess ? 0 : PMP_ECUDA;
+  }
+  if (ce <= cb) return cudaMemsetAsync(partial, 0, 16, st) == cudaSuccess ? 0 : PMP_ECUDA;
+  // level-2 nodes [qb, qe) and the index ranges of every upper level
+  uint64_t lo[kL + 1], hi[kL + 1];
+  lo[2] = cb / 128;
+  hi[2] = (ce + 127) / 128;
+  size_t total_vals = 0;
+  for (int j = 2; j <= gm.leff; j++) {
+    if (j > 2) {
+      lo[j] = lo[j - 1] / 128;
+      hi[j] = (hi[j - 1] + 127) / 128;
+    }
+    if (j < gm.leff) total_vals += hi[j] - lo[j];
+  }
+  Scratch sc(st);
+  if (total_vals && sc.alloc(total_vals * 16)) return PMP_ENOMEM;
+  uint64_t *buf = (uint64_t *)sc.p;
+  uint64_t *lvl[kL + 1];
+  size_t off = 0;
+  for (int j = 2; j <= gm.leff; j++) {
+    if (j == gm.leff) {
+      lvl[j] = partial;  // top level: exactly one node (index 0)
+    } else {
+      lvl[j] = buf + 2 * off;
+      off += hi[j] - lo[j];
+    }
+  }
+  {
+    const uint64_t nodes = hi[2] - lo[2];
+    const uint64_t maxgrid = (uint64_t)sms * 16;
+    uint64_t grid = (nodes + kWWarps - 1) / kWWarps;
+    if (grid > maxgrid) grid = maxgrid;
+    int rc = launch("k_node", st, [&] {
+      k_node<BITS><<<(unsigned)grid, kWWarps * 32, 0, st>>>(k->d_blob, s, cb, ce, lo[2], hi[2], 0, lvl[2]);
+    });
+    if (rc) return rc;
+  }
+  for (int j = 3; j <= gm.leff; j++) {
+    const uint64_t nodes = hi[j] - lo[j];
+    uint64_t grid = (nodes + kWWarps - 1) / kWWarps;
+    if (grid > (uint64_t)sms * 16) grid = (uint64_t)sms * 16;
+    int rc = launch("k_level", st, [&] {
+      k_level<BITS><<<(unsigned)grid, kWWarps * 32, 0, st>>>(k->d_blob, j, lvl[j - 1], lo[j - 1],
+                                                             hi[j - 1] - lo[j - 1], lvl[j], lo[j], nodes);
+    });
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char *pmp_strerror(int code) {
+  if (code > 0 || code < -5) return "unknown error";
+  return kErr[-code];
+}
+
+pmp_keys *pmp_keygen(uint64_t seed, int out_bits) {
+  if (out_bits != 32 && out_bits != 64) return nullptr;
+  pmp_keys *k = new (std::nothrow) pmp_keys;
+  if (!k) return nullptr;
+  k->bits = out_bits;
+  uint64_t sm = seed;
+  Xoshiro g;
+  for (int i = 0; i < 4; i++) g.s[i] = splitmix(sm);
+  const uint64_t amax = amax_of(out_bits);
+  for (uint32_t j = 0; j < kL; j++) {
+    uint64_t x = g.next();
+    k->b[j] = out_bits == 64 ? x : (x >> 32);
+    for (uint32_t i = 0; i < kM; i++) {
+      do {
+        x = g.next();
+        if (out_bits == 32) x >>= 32;
+      } while (x == 0 || x > amax);
+      k->a[j * kM + i] = x;
+    }
+  }
+  if (upload(k) != 0) {
+    delete k;
+    return nullptr;
+  }
+  return k;
+}
+
+pmp_keys *pmp_keys_from_words(int out_bits, const uint64_t *b, const uint64_t *a) {
+  if ((out_bits != 32 && out_bits != 64) || !b || !a) return nullptr;
+  const uint64_t amax = amax_of(out_bits);
+  for (uint32_t j = 0; j < kL; j++) {
+    if (out_bits == 32 && b[j] >> 32) return nullptr;
+    for (uint32_t i = 0; i < kM; i++)
+      if (a[j * kM + i] == 0 || a[j * kM + i] > amax) return nullptr;
+  }
+  pmp_keys *k = new (std::nothrow) pmp_keys;
+  if (!k) return nullptr;
+  k->bits = out_bits;
+  memcpy(k->b, b, sizeof(k->b));
+  memcpy(k->a, a, sizeof(k->a));
+  if (upload(k) != 0) {
+    delete k;
+    return nullptr;
+  }
+  return k;
+}
+
+int pmp_keys_export(const pmp_keys *k, uint64_t *b, uint64_t *a) {
+  if (!k || !b || !a) return PMP_EINVAL;
+  memcpy(b, k->b, sizeof(k->b));
+  memcpy(a, k->a, sizeof(k->a));
+  return 0;
+}
+
+int pmp_keys_bits(const pmp_keys *k) { return k ? k->bits : PMP_EINVAL; }
+
+void pmp_keys_free(pmp_keys *k) {
+  if (!k) return;
+  if (k->d_blob) cudaFree(k->d_blob);
+  delete k;
+}
+
+int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
+                   void *out, cudaStream_t st) {
+  if (!k) return PMP_EINVAL;
+  if (n == 0) return 0;
+  if (!bytes || !offsets || !out || n >= (1ULL << 32)) return PMP_EINVAL;
+  if (int rc = check_keys(k)) return rc;
+  const int sms = sm_count(k->device);
+  Scratch sc(st);
+  // work list (n u32) + counters [mid, big, next]
+  if (sc.alloc((size_t)n * 4 + 16)) return PMP_ENOMEM;
+  uint32_t *wcount = (uint32_t *)sc.p;
+  uint32_t *wlist = wcount + 4;
+  if (cudaMemsetAsync(wcount, 0, 16, st) != cudaSuccess) return PMP_ECUDA;
+  const ParamKeys pk = param_keys(k);
+  const uint64_t warps = (n + 31) / 32;
+  uint64_t grid = (warps + kShortWarps - 1) / kShortWarps;
+  const uint64_t maxgrid = (uint64_t)sms * 6;  // resident blocks (33 KB smem each)
+  if (grid > maxgrid) grid = maxgrid;
+  int rc;
+  if (k->bits == 64)
+    rc = launch("k_short", st, [&] { k_short<64><<<(unsigned)grid, kShortWarps * 32, 0, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
+  else
+    rc = launch("k_short", st, [&] { k_short<32><<<(unsigned)grid, kShortWarps * 32, 0, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
+  if (rc) return rc;
+  const unsigned wgrid = (unsigned)sms * 8;  // persistent, work list drained by atomics
+  if (k->bits == 64)
+    rc = launch("k_wstring", st, [&] { k_wstring<64><<<wgrid, kWWarps * 32, 0, st>>>(k->d_blob, bytes, offsets, n, out, wlist, wcount); });
+  else
+    rc = launch("k_wstring", st, [&] { k_wstring<32><<<wgrid, kWWarps * 32, 0, st>>>(k->d_blob, bytes, offsets, n, out, wlist, wcount); });
+  return rc;
+}
+
+int pmp_hash_long_partial(const pmp_keys *k, const uint8_t *local, uint64_t local_len, uint64_t g0,
+                          uint64_t total, uint64_t *partial, cudaStream_t st) {
+  if (!k || !partial || (!local && local_len > 0)) return PMP_EINVAL;
+  if (words_of(k->bits, total) > (1ULL << 56)) return PMP_ETOOLONG;
+  const uint64_t CB = (uint64_t)chunk_bytes(k->bits);
+  if (g0 % CB != 0 || g0 + local_len > total || g0 + local_len < g0) return PMP_EINVAL;
+  if (g0 + local_len != total && local_len % CB != 0) return PMP_EINVAL;
+  if (int rc = check_keys(k)) return rc;
+  return k->bits == 64 ? long_partial_impl<64>(k, local, local_len, g0, total, partial, st)
+                       : long_partial_impl<32>(k, local, local_len, g0, total, partial, st);
+}
+
+int pmp_hash_long_combine(const pmp_keys *k, const uint64_t *partials, int G, uint64_t total,
+                          void *out, cudaStream_t st) {
+  if (!k || !partials || !out || G < 1) return PMP_EINVAL;
+  if (int rc = check_keys(k)) return rc;
+  const u128 c = long_constant(k, total);
+  const uint64_t clo = (uint64_t)c, chi = (uint64_t)(c >> 64);
+  if (k->bits == 64)
+    return launch("k_combine", st, [&] { k_combine<64><<<1, 32, 0, st>>>(partials, G, clo, chi, out); });
+  return launch("k_combine", st, [&] { k_combine<32><<<1, 32, 0, st>>>(partials, G, clo, chi, out); });
+}
+
+int pmp_hash_long(const pmp_keys *k, const uint8_t *bytes, uint64_t len, void *out, cudaStream_t st) {
+  if (!k || !out || (!bytes && len > 0)) return PMP_EINVAL;
+  if (int rc = check_keys(k)) return rc;
+  Scratch sc(st);
+  if (sc.alloc(16)) return PMP_ENOMEM;
+  uint64_t *partial = (uint64_t *)sc.p;
+  int rc = pmp_hash_long_partial(k, bytes, len, 0, len, partial, st);
+  if (rc) return rc;
+  return pmp_hash_long_combine(k, partial, 1, len, out, st);
+}
+
+int pmp_long_split(int out_bits, uint64_t total, int G, uint64_t *begins) {
+  if ((out_bits != 32 && out_bits != 64) || G < 1 || !begins) return PMP_EINVAL;
+  const uint64_t CB = (uint64_t)chunk_bytes(out_bits);
+  const uint64_t full = total / CB;  // whole level-1 blocks present in the bytes
+  for (int g = 0; g < G; g++) begins[g] = (uint64_t)(((u128)full * (uint64_t)g) / (uint64_t)G) * CB;
+  begins[G] = total;
+  return 0;
+}
+
+int pmp_long_constant(const pmp_keys *k, uint64_t total, uint64_t *c2) {
+  if (!k || !c2) return PMP_EINVAL;
+  const u128 c = long_constant(k, total);
+  c2[0] = (uint64_t)c;
+  c2[1] = (uint64_t)(c >> 64);
+  return 0;
+}
+
+int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_t *out, cudaStream_t st) {
+  if ((out_bits != 32 && out_bits != 64) || mode < 0 || mode > 2 || (n && (!in || !out))) return PMP_EINVAL;
+  if (n == 0) return 0;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return PMP_ENODEV;
+  const unsigned grid = (unsigned)((n + 127) / 128);
+  if (out_bits == 64)
+    return launch("k_selftest", st, [&] { k_selftest<64><<<grid, 128, 0, st>>>(mode, in, n, out); });
+  return launch("k_selftest", st, [&] { k_selftest<32><<<grid, 128, 0, st>>>(mode, in, n, out); });
+}
+
+uint64_t pmp_launch_count(void) { return g_launches.load(); }
+
+void pmp_prof_enable(int on) { g_prof.store(on ? 1 : 0); }
+
+static void prof_drain() {
+  std::vector<ProfRec> pend;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    pend.swap(g_pending);
+  }
+  for (auto &r : pend) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    std::lock_guard<std::mutex> lk(g_mu);
+    bool found = false;
+    for (auto &d : g_done)
+      if (d.first == r.name) {
+        d.second.first += ms;
+        d.second.second += 1;
+        found = true;
+      }
+    if (!found) g_done.push_back({r.name, {ms, 1}});
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+}
+
+void pmp_prof_reset(void) {
+  prof_drain();
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_done.clear();
+}
+
+int pmp_prof_read(const char *prefix, double *ms, uint64_t *count) {
+  if (!prefix || !ms || !count) return PMP_EINVAL;
+  prof_drain();
+  std::lock_guard<std::mutex> lk(g_mu);
+  *ms = 0;
+  *count = 0;
+  const size_t pl = strlen(prefix);
+  for (auto &d : g_done)
+    if (d.first.compare(0, pl, prefix) == 0) {
+      *ms += d.second.first;
+      *count += d.second.second;
+    }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,268 @@
+// pmp_arith.cuh -- exact PM+ arithmetic on the sm_100a 32-bit integer pipes.
+//
+// Independent of oracle/ (shares no code); checked against it end to end.
+// Citations: P:n = PAPER.md line n (arXiv:1609.09840 LaTeX), S:n = SPEC.md.
+//
+//  * Exact chunk sums: S = b + sum_{i<128} a_i s_i is never reduced
+//    inside a chunk ("one modulo per m products").  PM+64: S < 2^135, held
+//    in five 32-bit limbs; PM+32: S < 2^71, three limbs.
+//  * The hot-loop accumulator is a redundant carry-save form (MacAcc64): the four
+//    32x32->64 partial products of a 64x64 product go to three 64-bit
+//    accumulators at weights 2^0, 2^32, 2^64, each with its own carry counter, so
+//    every product is one IMAD.WIDE.U32 (carry out) + one IADD3.X, with no carry
+//    chain across limbs.  Normalised to exact limbs once per lane per chunk.
+//  * 3-word -> 2-word reduction: S == (w0 + k^2 w2 + k u1) + (2^n + k - u0)
+//    with k w1 = u1 2^n + u0; then Algorithm 2 with the v1 = 2 branch
+//    read as 2^n + v0 - k (prose P:690-691; reading Q6 -- the printed "v0 - k" is
+//    a misprint).
+//  * Field elements at levels >= 2 are (lo, hi) with hi in {0,1}; the
+//    products a * v fit in 2n bits because a <= p - kappa - 1 (reading Q7).
+//  * Finaliser: V mod 2^n = lo, then the mixer of P:722-734.
+#pragma once
+#include <stdint.h>
+
+#define PMP_DI __device__ __forceinline__
+#define PMP_HDI __host__ __device__ __forceinline__
+
+namespace pmp {
+
+constexpr uint32_t kM = 128;    // block width m (Table 2)
+constexpr uint32_t kL = 8;      // levels L
+constexpr uint64_t kK64 = 13;   // p = 2^64 + 13
+constexpr uint64_t kK32 = 15;   // p = 2^32 + 15
+
+// ----------------------------------------------------------------- finaliser
+PMP_HDI uint64_t mix64(uint64_t z) {
+  z ^= z >> 33;
+  z *= 0xc4ceb9fe1a85ec53ULL;
+  z ^= z >> 33;
+  return z;
+}
+PMP_HDI uint32_t mix32(uint32_t z) {
+  z ^= z >> 13;
+  z *= 0xab3be54fU;
+  z ^= z >> 16;
+  return z;
+}
+
+// ----------------------------------------------------------------- PM+64
+struct Fe64 {        // value lo + hi * 2^64 in [0, p), hi in {0,1}
+  uint64_t lo;
+  uint32_t hi;
+};
+
+struct Acc5 {        // exact value c0 + c1 2^32 + ... + c4 2^128
+  uint32_t c0, c1, c2, c3, c4;
+};
+
+struct MacAcc64 {    // carry-save: (L1:L0) + cL 2^64 + ((M1:M0) + cM 2^64) 2^32 + ((H1:H0) + cH 2^64) 2^64
+  uint32_t L0, L1, cL, M0, M1, cM, H0, H1, cH;
+};
+
+PMP_DI void macc_zero(MacAcc64 &A) {
+  A.L0 = A.L1 = A.cL = A.M0 = A.M1 = A.cM = A.H0 = A.H1 = A.cH = 0;
+}
+
+// A += a * s  (a, s < 2^64).  Two SASS ops per 32x32 partial product.
+PMP_DI void mac64(MacAcc64 &A, uint32_t a0, uint32_t a1, uint32_t s0, uint32_t s1) {
+  asm("mad.lo.cc.u32  %0, %9, %11, %0;\n\t"
+      "madc.hi.cc.u32 %1, %9, %11, %1;\n\t"
+      "addc.u32       %2, %2, 0;\n\t"
+      "mad.lo.cc.u32  %3, %9, %12, %3;\n\t"
+      "madc.hi.cc.u32 %4, %9, %12, %4;\n\t"
+      "addc.u32       %5, %5, 0;\n\t"
+      "mad.lo.cc.u32  %3, %10, %11, %3;\n\t"
+      "madc.hi.cc.u32 %4, %10, %11, %4;\n\t"
+      "addc.u32       %5, %5, 0;\n\t"
+      "mad.lo.cc.u32  %6, %10, %12, %6;\n\t"
+      "madc.hi.cc.u32 %7, %10, %12, %7;\n\t"
+      "addc.u32       %8, %8, 0;"
+      : "+r"(A.L0), "+r"(A.L1), "+r"(A.cL), "+r"(A.M0), "+r"(A.M1), "+r"(A.cM),
+        "+r"(A.H0), "+r"(A.H1), "+r"(A.cH)
+      : "r"(a0), "r"(a1), "r"(s0), "r"(s1));
+}
+PMP_DI void mac64(MacAcc64 &A, uint64_t a, uint64_t s) {
+  mac64(A, (uint32_t)a, (uint32_t)(a >> 32), (uint32_t)s, (uint32_t)(s >> 32));
+}
+
+// carry-save -> exact limbs (value unchanged)
+PMP_DI Acc5 macc_normalize(const MacAcc64 &A) {
+  Acc5 r;
+  r.c0 = A.L0;
+  asm("add.cc.u32  %0, %5, %6;\n\t"     // c1 = L1 + M0
+      "addc.cc.u32 %1, %7, %8;\n\t"     // c2 = M1 + H0 + cy
+      "addc.cc.u32 %2, %9, %10;\n\t"    // c3 = H1 + cM + cy
+      "addc.u32    %3, %11, 0;\n\t"     // c4 = cH + cy
+      "add.cc.u32  %1, %1, %4;\n\t"     // c2 += cL
+      "addc.cc.u32 %2, %2, 0;\n\t"
+      "addc.u32    %3, %3, 0;"
+      : "=r"(r.c1), "=r"(r.c2), "=r"(r.c3), "=r"(r.c4)
+      : "r"(A.cL), "r"(A.L1), "r"(A.M0), "r"(A.M1), "r"(A.H0), "r"(A.H1), "r"(A.cM),
+        "r"(A.cH));
+  return r;
+}
+
+PMP_DI void acc5_add(Acc5 &x, const Acc5 &y) {
+  asm("add.cc.u32  %0, %0, %5;\n\t"
+      "addc.cc.u32 %1, %1, %6;\n\t"
+      "addc.cc.u32 %2, %2, %7;\n\t"
+      "addc.cc.u32 %3, %3, %8;\n\t"
+      "addc.u32    %4, %4, %9;"
+      : "+r"(x.c0), "+r"(x.c1), "+r"(x.c2), "+r"(x.c3), "+r"(x.c4)
+      : "r"(y.c0), "r"(y.c1), "r"(y.c2), "r"(y.c3), "r"(y.c4));
+}
+
+PMP_DI void acc5_add_u64(Acc5 &x, uint64_t v) {  // x += v (v < 2^64)
+  asm("add.cc.u32  %0, %0, %5;\n\t"
+      "addc.cc.u32 %1, %1, %6;\n\t"
+      "addc.cc.u32 %2, %2, 0;\n\t"
+      "addc.cc.u32 %3, %3, 0;\n\t"
+      "addc.u32    %4, %4, 0;"
+      : "+r"(x.c0), "+r"(x.c1), "+r"(x.c2), "+r"(x.c3), "+r"(x.c4)
+      : "r"((uint32_t)v), "r"((uint32_t)(v >> 32)));
+}
+
+// x += a * v for a field element v (mul_field): a*lo + (hi ? a 2^64 : 0)
+PMP_DI void acc5_mac_fe(Acc5 &x, uint64_t a, const Fe64 &v) {
+  uint64_t plo = a * v.lo;
+  uint64_t phi = __umul64hi(a, v.lo);
+  uint64_t ahi = v.hi ? a : 0ULL;
+  asm("add.cc.u32  %0, %0, %5;\n\t"
+      "addc.cc.u32 %1, %1, %6;\n\t"
+      "addc.cc.u32 %2, %2, %7;\n\t"
+      "addc.cc.u32 %3, %3, %8;\n\t"
+      "addc.u32    %4, %4, 0;\n\t"
+      "add.cc.u32  %2, %2, %9;\n\t"
+      "addc.cc.u32 %3, %3, %10;\n\t"
+      "addc.u32    %4, %4, 0;"
+      : "+r"(x.c0), "+r"(x.c1), "+r"(x.c2), "+r"(x.c3), "+r"(x.c4)
+      : "r"((uint32_t)plo), "r"((uint32_t)(plo >> 32)), "r"((uint32_t)phi),
+        "r"((uint32_t)(phi >> 32)), "r"((uint32_t)ahi), "r"((uint32_t)(ahi >> 32)));
+}
+
+PMP_DI Acc5 acc5_shfl_xor(const Acc5 &x, int m) {
+  Acc5 r;
+  r.c0 = __shfl_xor_sync(0xffffffffu, x.c0, m);
+  r.c1 = __shfl_xor_sync(0xffffffffu, x.c1, m);
+  r.c2 = __shfl_xor_sync(0xffffffffu, x.c2, m);
+  r.c3 = __shfl_xor_sync(0xffffffffu, x.c3, m);
+  r.c4 = __shfl_xor_sync(0xffffffffu, x.c4, m);
+  return r;
+}
+
+// Section 6.2: S = w0 + w1 2^64 + w2 2^128 -> (v0, v1), v1 <= 2
+PMP_HDI void reduce3to2_64(uint64_t w0, uint64_t w1, uint64_t w2, uint64_t &v0, uint32_t &v1) {
+#ifdef __CUDA_ARCH__
+  uint64_t u1 = __umul64hi(w1, kK64);
+#else
+  uint64_t u1 = (uint64_t)(((unsigned __int128)w1 * kK64) >> 64);
+#endif
+  uint64_t u0 = w1 * kK64;                              // k w1 = u1 2^64 + u0
+  uint64_t t = kK64 * kK64 * w2 + kK64 * u1;            // k^2 w2 + k u1 (< 2^40)
+  uint64_t x0 = w0 + t;                                 // X = w0 + k^2 w2 + k u1
+  uint32_t x1 = x0 < t;
+  uint64_t y0 = kK64 - u0;                              // Y = 2^64 + k - u0
+  uint32_t y1 = u0 <= kK64;
+  v0 = x0 + y0;
+  v1 = x1 + y1 + (uint32_t)(v0 < x0);
+}
+
+// Algorithm 2, v1 = 2 branch corrected (reading Q6).
+PMP_HDI Fe64 alg2_64(uint64_t v0, uint32_t v1) {
+  Fe64 z;
+  if (kK64 * v1 <= v0) {                 // line 2-3: v0 - k v1
+    z.lo = v0 - kK64 * v1;
+    z.hi = 0;
+  } else if (v1 == 1) {                  // line 4-5: v0 + 2^n (v0 < k)
+    z.lo = v0;
+    z.hi = 1;
+  } else {                               // v1 == 2: 2^n + v0 - k (v0 < 2k)
+    z.lo = v0 - kK64;
+    z.hi = v0 >= kK64;
+  }
+  return z;
+}
+
+PMP_HDI Fe64 reduce_acc5(const Acc5 &x) {
+  uint64_t w0 = ((uint64_t)x.c1 << 32) | x.c0;
+  uint64_t w1 = ((uint64_t)x.c3 << 32) | x.c2;
+  uint64_t v0;
+  uint32_t v1;
+  reduce3to2_64(w0, w1, x.c4, v0, v1);
+  return alg2_64(v0, v1);
+}
+
+// ----------------------------------------------------------------- PM+32
+struct Acc3 {        // exact value c0 + c1 2^32 + c2 2^64
+  uint32_t c0, c1, c2;
+};
+
+PMP_DI void mac32(Acc3 &A, uint32_t a, uint32_t s) {  // one IMAD.WIDE.U32 + one IADD3.X
+  asm("mad.lo.cc.u32  %0, %3, %4, %0;\n\t"
+      "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+      "addc.u32       %2, %2, 0;"
+      : "+r"(A.c0), "+r"(A.c1), "+r"(A.c2)
+      : "r"(a), "r"(s));
+}
+
+PMP_DI void acc3_add(Acc3 &x, const Acc3 &y) {
+  asm("add.cc.u32  %0, %0, %3;\n\t"
+      "addc.cc.u32 %1, %1, %4;\n\t"
+      "addc.u32    %2, %2, %5;"
+      : "+r"(x.c0), "+r"(x.c1), "+r"(x.c2)
+      : "r"(y.c0), "r"(y.c1), "r"(y.c2));
+}
+
+PMP_DI void acc3_add_u64(Acc3 &x, uint64_t v) {
+  asm("add.cc.u32  %0, %0, %3;\n\t"
+      "addc.cc.u32 %1, %1, %4;\n\t"
+      "addc.u32    %2, %2, 0;"
+      : "+r"(x.c0), "+r"(x.c1), "+r"(x.c2)
+      : "r"((uint32_t)v), "r"((uint32_t)(v >> 32)));
+}
+
+// x += a * v, v < p = 2^32 + 15 held in a u64 (lo 32 bits + hi bit)
+PMP_DI void acc3_mac_fe(Acc3 &x, uint32_t a, uint64_t v) {
+  uint64_t prod = (uint64_t)a * (uint32_t)v;
+  uint32_t ahi = (v >> 32) ? a : 0u;
+  asm("add.cc.u32  %0, %0, %3;\n\t"
+      "addc.cc.u32 %1, %1, %4;\n\t"
+      "addc.u32    %2, %2, 0;\n\t"
+      "add.cc.u32  %1, %1, %5;\n\t"
+      "addc.u32    %2, %2, 0;"
+      : "+r"(x.c0), "+r"(x.c1), "+r"(x.c2)
+      : "r"((uint32_t)prod), "r"((uint32_t)(prod >> 32)), "r"(ahi));
+}
+
+PMP_DI Acc3 acc3_shfl_xor(const Acc3 &x, int m) {
+  Acc3 r;
+  r.c0 = __shfl_xor_sync(0xffffffffu, x.c0, m);
+  r.c1 = __shfl_xor_sync(0xffffffffu, x.c1, m);
+  r.c2 = __shfl_xor_sync(0xffffffffu, x.c2, m);
+  return r;
+}
+
+// Section 6.2 for n = 32, k = 15: (v0, v1) with v1 <= 2 for w2 < 2^24
+PMP_HDI void reduce3to2_32(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t &v0, uint32_t &v1) {
+  uint64_t u = (uint64_t)w1 * kK32;                     // u1 2^32 + u0
+  uint64_t u0 = (uint32_t)u, u1 = u >> 32;
+  uint64_t x = (uint64_t)w0 + kK32 * kK32 * w2 + kK32 * u1;
+  uint64_t y = (1ULL << 32) + kK32 - u0;
+  uint64_t v = x + y;
+  v0 = (uint32_t)v;
+  v1 = (uint32_t)(v >> 32);
+}
+
+PMP_HDI uint64_t alg2_32(uint32_t v0, uint32_t v1) {  // Algorithm 2 (corrected), value < p
+  if (kK32 * v1 <= v0) return (uint64_t)v0 - kK32 * v1;
+  if (v1 == 1) return (1ULL << 32) + v0;
+  return (1ULL << 32) + v0 - kK32;
+}
+
+PMP_HDI uint64_t reduce_acc3(const Acc3 &x) {
+  uint32_t v0, v1;
+  reduce3to2_32(x.c0, x.c1, x.c2, v0, v1);
+  return alg2_32(v0, v1);
+}
+
+}  // namespace pmp

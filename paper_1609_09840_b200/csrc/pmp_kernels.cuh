@@ -1,0 +1,670 @@
+// pmp_kernels.cuh -- PM+ hot-path kernels for sm_100a.
+//
+// Layout of the work:
+//   k_short   thread per string for strings <= kShortMax bytes (one level-1
+//             block, T <= 16 / 32 words).  A warp stages the contiguous byte
+//             span of its 32 strings into shared memory with coalesced 16-byte
+//             loads, then each lane walks its own string.  Strings longer than
+//             kShortMax are appended to a work list for k_wstring.
+//   k_wstring warp per string (from the work list): chunk-parallel level 1 with
+//             8 lanes per chunk, fused level 2, streaming upper levels.
+//   k_node    warp per level-2 node of one long string (pmp_hash_long*):
+//             partial level-2 sums s2 = sum_r a_{2,r} v1 over the caller's chunks.
+//   k_level   warp per node of level j >= 3 over partial sums.
+//   k_combine sums the rank partials + the key-only constant, finalises.
+//
+// Citations: P:n = PAPER.md line n.  Eq. (1); Algorithm 1 P:427-443;
+// byte packing P:456; reduction P:659-709; finaliser P:722-734.
+#pragma once
+#include <stdint.h>
+#include "pmp_arith.cuh"
+
+namespace pmp {
+
+constexpr uint32_t kShortMax = 127;      // bytes; k_short handles B <= kShortMax
+constexpr uint32_t kBigBytes = 1u << 16; // work-list class "big" (processed first)
+constexpr int kShortWarps = 8;           // warps per k_short block
+constexpr int kStageUnits = 264;         // 16-byte units of staging per warp (>= 32*127+15+132 bytes)
+constexpr int kWWarps = 4;               // warps per k_wstring / k_node block
+constexpr uint32_t FULL = 0xffffffffu;
+
+// level-1 keys 0..31 and b_1 passed by value: they live in the constant bank
+// and become immediate operands of the multiply-adds in k_short.
+struct ParamKeys {
+  uint64_t a[32];
+  uint64_t b;
+};
+
+// ------------------------------------------------------------- helpers
+PMP_DI uint4 ld_stream16(const void *p) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+PMP_DI uint32_t ld_u32(const void *p) {
+  uint32_t r;
+  asm("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+PMP_DI uint32_t funnel(uint32_t lo, uint32_t hi, uint32_t sh) { return __funnelshift_r(lo, hi, sh); }
+
+// ------------------------------------------------------------- width traits
+template <int BITS> struct Tr;
+template <> struct Tr<64> {
+  using Acc = Acc5;
+  using Fe = Fe64;
+  using Key = uint64_t;
+  static constexpr int W = 8;            // bytes per word
+  static constexpr int CHUNK = 1024;     // bytes per level-1 block (128 words)
+  static constexpr int CPG = 1;          // chunks per 1 KiB group block
+};
+template <> struct Tr<32> {
+  using Acc = Acc3;
+  using Fe = uint64_t;
+  using Key = uint32_t;
+  static constexpr int W = 4;
+  static constexpr int CHUNK = 512;
+  static constexpr int CPG = 2;
+};
+
+PMP_DI void acc_zero(Acc5 &x) { x.c0 = x.c1 = x.c2 = x.c3 = x.c4 = 0; }
+PMP_DI void acc_zero(Acc3 &x) { x.c0 = x.c1 = x.c2 = 0; }
+PMP_DI void acc_add(Acc5 &x, const Acc5 &y) { acc5_add(x, y); }
+PMP_DI void acc_add(Acc3 &x, const Acc3 &y) { acc3_add(x, y); }
+PMP_DI void acc_add_word(Acc5 &x, uint64_t v) { acc5_add_u64(x, v); }
+PMP_DI void acc_add_word(Acc3 &x, uint64_t v) { acc3_add_u64(x, v); }
+PMP_DI void acc_mac_fe(Acc5 &x, uint64_t a, const Fe64 &v) { acc5_mac_fe(x, a, v); }
+PMP_DI void acc_mac_fe(Acc3 &x, uint64_t a, uint64_t v) { acc3_mac_fe(x, (uint32_t)a, v); }
+PMP_DI void acc_add_fe(Acc5 &x, const Fe64 &v) {  // x += v (field element, < 2^65)
+  acc5_add_u64(x, v.lo);
+  Acc5 h = {0, 0, v.hi, 0, 0};
+  acc5_add(x, h);
+}
+PMP_DI void acc_add_fe(Acc3 &x, uint64_t v) { acc3_add_u64(x, v); }
+PMP_DI Acc5 acc_shfl_xor(const Acc5 &x, int m) { return acc5_shfl_xor(x, m); }
+PMP_DI Acc3 acc_shfl_xor(const Acc3 &x, int m) { return acc3_shfl_xor(x, m); }
+PMP_DI Fe64 acc_reduce(const Acc5 &x) { return reduce_acc5(x); }
+PMP_DI uint64_t acc_reduce(const Acc3 &x) { return reduce_acc3(x); }
+PMP_DI uint64_t fe_lo(const Fe64 &v) { return v.lo; }
+PMP_DI uint64_t fe_lo(uint64_t v) { return (uint32_t)v; }
+PMP_DI void fe_store(uint64_t *dst, const Fe64 &v) { dst[0] = v.lo; dst[1] = v.hi; }
+PMP_DI void fe_store(uint64_t *dst, uint64_t v) { dst[0] = v; dst[1] = 0; }
+PMP_DI void fe_load(const uint64_t *src, Fe64 &v) { v.lo = src[0]; v.hi = (uint32_t)src[1]; }
+PMP_DI void fe_load(const uint64_t *src, uint64_t &v) { v = src[0]; }
+PMP_DI Fe64 fe_shfl(const Fe64 &v, int lane) {
+  Fe64 r;
+  r.lo = __shfl_sync(FULL, v.lo, lane);
+  r.hi = __shfl_sync(FULL, v.hi, lane);
+  return r;
+}
+PMP_DI uint64_t fe_shfl(uint64_t v, int lane) { return __shfl_sync(FULL, v, lane); }
+PMP_DI Fe64 fe_from_word(uint64_t w, Fe64 *) { Fe64 r; r.lo = w; r.hi = 0; return r; }
+PMP_DI uint64_t fe_from_word(uint64_t w, uint64_t *) { return w; }
+
+template <int BITS> PMP_DI void store_digest(void *out, uint64_t i, uint64_t lo);
+template <> PMP_DI void store_digest<64>(void *out, uint64_t i, uint64_t lo) {
+  reinterpret_cast<uint64_t *>(out)[i] = mix64(lo);
+}
+template <> PMP_DI void store_digest<32>(void *out, uint64_t i, uint64_t lo) {
+  reinterpret_cast<uint32_t *>(out)[i] = mix32((uint32_t)lo);
+}
+
+// ============================================================= k_short
+// One short string (B <= kShortMax, so T = floor(B/w)+1 <= 16 / 32 words and
+// the tree is a single f_1 block, or no block at all when T == 1).
+// `p` points at the aligned 32-bit word containing the first byte, `sh` is the
+// bit offset of that byte; words are read with `fetch(k)` (4-byte units).
+template <int BITS, class Fetch>
+PMP_DI uint64_t short_tree_lo(const ParamKeys &K, uint32_t B, uint32_t sh, int tmax, Fetch fetch) {
+  if constexpr (BITS == 64) {
+    const uint32_t tlast = B >> 3, r = B & 7;                 // word T-1 holds the marker
+    const uint64_t lmask = (1ULL << (8 * r)) - 1, marker = 1ULL << (8 * r);
+    MacAcc64 A;
+    macc_zero(A);
+    uint64_t sigma0 = 0;
+    uint32_t y0 = fetch(0);
+#pragma unroll
+    for (int t = 0; t < 16; t++) {
+      if (t > tmax) break;
+      uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
+      uint64_t w = ((uint64_t)funnel(y1, y2, sh) << 32) | funnel(y0, y1, sh);
+      y0 = y2;
+      if (t == (int)tlast) w = (w & lmask) | marker;
+      if (t == 0) sigma0 = w;
+      if (t <= (int)tlast) mac64(A, K.a[t], w);                // Eq. (1), lazy
+    }
+    if (tlast == 0) return sigma0;                             // |sigma| = 1: no f_j (reading Q2)
+    Acc5 x = macc_normalize(A);
+    acc5_add_u64(x, K.b);
+    return reduce_acc5(x).lo;                                  // mod p, then mod 2^64
+  } else {
+    const uint32_t tlast = B >> 2, r = B & 3;
+    const uint32_t lmask = (1u << (8 * r)) - 1, marker = 1u << (8 * r);
+    Acc3 A = {0, 0, 0};
+    uint32_t sigma0 = 0;
+    uint32_t y0 = fetch(0);
+#pragma unroll
+    for (int t = 0; t < 32; t++) {
+      if (t > tmax) break;
+      uint32_t y1 = fetch(t + 1);
+      uint32_t w = funnel(y0, y1, sh);
+      y0 = y1;
+      if (t == (int)tlast) w = (w & lmask) | marker;
+      if (t == 0) sigma0 = w;
+      if (t <= (int)tlast) mac32(A, (uint32_t)K.a[t], w);
+    }
+    if (tlast == 0) return sigma0;
+    acc3_add_u64(A, K.b);
+    return (uint32_t)reduce_acc3(A);
+  }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kShortWarps * 32)
+k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets,
+        uint64_t n, void *__restrict__ out, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
+  __shared__ uint4 stage_all[kShortWarps][kStageUnits];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint4 *stage = stage_all[wib];
+  const uint32_t *stage32 = reinterpret_cast<const uint32_t *>(stage);
+  const uint64_t gstride = (uint64_t)gridDim.x * kShortWarps * 32;
+  for (uint64_t base = ((uint64_t)blockIdx.x * kShortWarps + wib) * 32; base < n; base += gstride) {
+    const uint64_t i = base + lane;
+    const bool valid = i < n;
+    uint64_t o0 = 0, o1 = 0;
+    if (valid) {
+      o0 = offsets[i];
+      o1 = offsets[i + 1];
+    }
+    const uint64_t B = o1 - o0;
+    const bool is_short = valid && B <= kShortMax;
+    const bool is_long = valid && !is_short;
+    const unsigned longmask = __ballot_sync(FULL, is_long);
+    if (longmask) {
+      // warp-aggregated append: big strings from the back, others from the front
+      const bool big = is_long && B >= kBigBytes;
+      const unsigned bigmask = __ballot_sync(FULL, big), midmask = longmask & ~bigmask;
+      uint32_t mbase = 0, bbase = 0;
+      if (lane == 0) {
+        if (midmask) mbase = atomicAdd(&wcount[0], (uint32_t)__popc(midmask));
+        if (bigmask) bbase = atomicAdd(&wcount[1], (uint32_t)__popc(bigmask));
+      }
+      mbase = __shfl_sync(FULL, mbase, 0);
+      bbase = __shfl_sync(FULL, bbase, 0);
+      const unsigned lt = (1u << lane) - 1;
+      if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
+      if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
+    }
+    int tmax = 0;  // warp max of the marker word index
+    if (is_short) tmax = (int)(B / (BITS / 8));
+    tmax = (int)__reduce_max_sync(FULL, (unsigned)tmax);
+    uint64_t lo = 0;
+    if (longmask == 0) {
+      // all strings short: stage the warp's contiguous byte span [first, end)
+      const int last = 31 - __clz(__ballot_sync(FULL, valid));
+      const uint64_t first = __shfl_sync(FULL, o0, 0);
+      const uint64_t endo = __shfl_sync(FULL, o1, last);
+      const uintptr_t alo = (uintptr_t)(bytes + first) & ~(uintptr_t)15;
+      const uintptr_t ahi = ((uintptr_t)(bytes + endo) + 15) & ~(uintptr_t)15;
+      const int nunits = first < endo ? (int)((ahi - alo) >> 4) : 0;
+      uint4 tmp[9];
+#pragma unroll
+      for (int k = 0; k < 9; k++) {
+        const int u = lane + 32 * k;
+        if (u < nunits) tmp[k] = ld_stream16(reinterpret_cast<const void *>(alo + 16 * (uintptr_t)u));
+      }
+#pragma unroll
+      for (int k = 0; k < 9; k++) {
+        const int u = lane + 32 * k;
+        if (u < nunits) stage[u] = tmp[k];
+      }
+      __syncwarp();
+      if (is_short) {
+        const uint32_t s = (uint32_t)((uintptr_t)(bytes + o0) - alo);
+        const uint32_t *p = stage32 + (s >> 2);
+        lo = short_tree_lo<BITS>(K, (uint32_t)B, 8 * (s & 3), tmax, [&](int k) { return p[k]; });
+      }
+      __syncwarp();
+    } else if (is_short) {
+      // mixed warp: read the string's aligned 32-bit words straight from global,
+      // touching only words that overlap [start, end) (never past offsets[n]).
+      const uintptr_t sa = (uintptr_t)(bytes + o0), se = (uintptr_t)(bytes + o1);
+      const uintptr_t pa = sa & ~(uintptr_t)3;
+      lo = short_tree_lo<BITS>(K, (uint32_t)B, 8 * (uint32_t)(sa & 3), tmax, [&](int k) {
+        const uintptr_t a = pa + 4 * (uintptr_t)k;
+        return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
+      });
+    }
+    if (is_short) store_digest<BITS>(out, i, lo);
+  }
+}
+
+// ============================================================= warp chunk engine
+// A warp walks a range of level-1 chunks of one string, 4 KiB per iteration:
+// lane group g = lane/8 owns a 1 KiB group block (1 chunk for PM+64, 2 for
+// PM+32), lane r = lane%8 loads units r, r+8, ..., r+56 of it (each load
+// instruction covers four whole 128-byte lines).  Each lane multiply-adds its
+// 16 words against 16 level-1 keys held in registers, the 8 lanes of a group
+// combine their exact partial sums with 3 shuffle levels, add b_1, reduce mod p
+// (v_1 of the chunk, Eq. (1)), and fold a_{2, c mod 128} * v_1 into the
+// group's exact level-2 accumulator.
+template <int BITS> struct LaneKeys;
+template <> struct LaneKeys<64> {
+  uint64_t k[16];
+  PMP_DI void load(const uint64_t *a1, int r) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      k[2 * j] = a1[2 * (r + 8 * j)];
+      k[2 * j + 1] = a1[2 * (r + 8 * j) + 1];
+    }
+  }
+};
+template <> struct LaneKeys<32> {
+  uint32_t k[16];
+  PMP_DI void load(const uint64_t *a1, int r) {
+#pragma unroll
+    for (int jj = 0; jj < 4; jj++)
+#pragma unroll
+      for (int h = 0; h < 4; h++) k[4 * jj + h] = (uint32_t)a1[4 * (r + 8 * jj) + h];
+  }
+};
+
+struct StrView {
+  const uint8_t *base;  // byte at global offset g0 of the string
+  uint64_t g0;          // global byte offset of `base` (multiple of the chunk size)
+  uint64_t avail_end;   // global offset one past the last byte readable from `base`
+  uint64_t B;           // total string length (bytes)
+  uint32_t delta;       // (uintptr)base & 15
+};
+
+PMP_DI uint4 realign16(const uint4 &c, const uint4 &n, uint32_t q, uint32_t sh) {
+  const uint32_t y0 = q == 0 ? c.x : q == 1 ? c.y : q == 2 ? c.z : c.w;
+  const uint32_t y1 = q == 0 ? c.y : q == 1 ? c.z : q == 2 ? c.w : n.x;
+  const uint32_t y2 = q == 0 ? c.z : q == 1 ? c.w : q == 2 ? n.x : n.y;
+  const uint32_t y3 = q == 0 ? c.w : q == 1 ? n.x : q == 2 ? n.y : n.z;
+  const uint32_t y4 = q == 0 ? n.x : q == 1 ? n.y : q == 2 ? n.z : n.w;
+  uint4 r;
+  r.x = funnel(y0, y1, sh);
+  r.y = funnel(y1, y2, sh);
+  r.z = funnel(y2, y3, sh);
+  r.w = funnel(y3, y4, sh);
+  return r;
+}
+
+// Loads the 8 units of this lane for the group block starting at global byte
+// offset `gofs`, realigned to the string's byte 0, zero where unavailable.
+PMP_DI void load_group_block(const StrView &s, uint64_t gofs, int lane, uint4 (&U)[8]) {
+  const int r = lane & 7;
+  if (s.delta == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const uint64_t off = gofs + 16 * (uint64_t)(r + 8 * j);
+      U[j] = off < s.avail_end ? ld_stream16(s.base + (off - s.g0)) : make_uint4(0, 0, 0, 0);
+    }
+  } else {
+    // aligned unit k covers string-relative bytes [16k - delta, 16k - delta + 16)
+    const uint8_t *abase = s.base - s.delta;
+    uint4 X[9];
+#pragma unroll
+    for (int j = 0; j < 9; j++) {
+      const uint64_t off = gofs + 16 * (uint64_t)(r + 8 * j);
+      const bool need = (j < 8) || (r == 0);
+      X[j] = (need && off < s.avail_end + s.delta) ? ld_stream16(abase + (off - s.g0))
+                                                   : make_uint4(0, 0, 0, 0);
+    }
+    const uint32_t q = s.delta >> 2, sh = 8 * (s.delta & 3);
+    const int src = (lane & ~7) | ((r + 1) & 7);
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const uint4 send = r == 0 ? X[j + 1] : X[j];  // lane r needs aligned unit r+8j+1
+      uint4 nx;
+      nx.x = __shfl_sync(FULL, send.x, src);
+      nx.y = __shfl_sync(FULL, send.y, src);
+      nx.z = __shfl_sync(FULL, send.z, src);
+      nx.w = __shfl_sync(FULL, send.w, src);
+      U[j] = realign16(X[j], nx, q, sh);
+    }
+  }
+}
+
+// sigma word fix-up near the end of the string: word tlast carries the
+// 0x01 marker after the last data byte; words past it are the zero padding.
+template <int BITS>
+PMP_DI void fixup_unit(uint4 &u, uint64_t t0, uint64_t tlast, uint32_t rbytes) {
+  if constexpr (BITS == 64) {
+    uint64_t w[2] = {((uint64_t)u.y << 32) | u.x, ((uint64_t)u.w << 32) | u.z};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint64_t t = t0 + h;
+      if (t == tlast) w[h] = (w[h] & ((1ULL << (8 * rbytes)) - 1)) | (1ULL << (8 * rbytes));
+      else if (t > tlast) w[h] = 0;
+    }
+    u = make_uint4((uint32_t)w[0], (uint32_t)(w[0] >> 32), (uint32_t)w[1], (uint32_t)(w[1] >> 32));
+  } else {
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+      const uint64_t t = t0 + h;
+      if (t == tlast) w[h] = (w[h] & ((1u << (8 * rbytes)) - 1)) | (1u << (8 * rbytes));
+      else if (t > tlast) w[h] = 0;
+    }
+    u = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+template <int BITS> struct ChunkOut {
+  typename Tr<BITS>::Acc acc2;  // sum over processed chunks of a_{2,c mod 128} * v_1(c)
+  typename Tr<BITS>::Fe v1_first;  // v_1 of chunk cb (for the single-chunk tree)
+};
+
+// Processes chunks [cb, ce) (all inside one level-2 node).  Every lane returns
+// the same values.
+template <int BITS>
+PMP_DI ChunkOut<BITS> warp_chunks(const StrView &s, uint64_t cb, uint64_t ce, const LaneKeys<BITS> &lk,
+                                  uint64_t b1, const uint64_t *__restrict__ a2, int lane) {
+  using T = Tr<BITS>;
+  using Acc = typename T::Acc;
+  using Fe = typename T::Fe;
+  constexpr int CPG = T::CPG, CPI = 4 * CPG, W = T::W;
+  const int g = lane >> 3, r = lane & 7;
+  const uint64_t tlast = s.B / W;             // index of the marker word, T - 1
+  const uint32_t rbytes = (uint32_t)(s.B % W);
+  ChunkOut<BITS> res;
+  acc_zero(res.acc2);
+  res.v1_first = Fe();
+  for (uint64_t c0 = cb; c0 < ce; c0 += CPI) {
+    const uint64_t gofs = (c0 + (uint64_t)g * CPG) * (uint64_t)T::CHUNK;  // group block start
+    uint4 U[8];
+    load_group_block(s, gofs, lane, U);
+    const bool tail = tlast < (c0 + CPI) * 128;  // warp-uniform
+    if (tail) {
+#pragma unroll
+      for (int j = 0; j < 8; j++) fixup_unit<BITS>(U[j], (gofs + 16 * (uint64_t)(r + 8 * j)) / W, tlast, rbytes);
+    }
+    // ---- level-1 multiply-accumulate (the hot loop) ----
+    Acc part[CPG];
+    if constexpr (BITS == 64) {
+      MacAcc64 A;
+      macc_zero(A);
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        mac64(A, (uint32_t)lk.k[2 * j], (uint32_t)(lk.k[2 * j] >> 32), U[j].x, U[j].y);
+        mac64(A, (uint32_t)lk.k[2 * j + 1], (uint32_t)(lk.k[2 * j + 1] >> 32), U[j].z, U[j].w);
+      }
+      part[0] = macc_normalize(A);
+    } else {
+      Acc3 A[2] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int cs = j >> 2, kb = 4 * (j & 3);
+        mac32(A[cs], lk.k[kb + 0], U[j].x);
+        mac32(A[cs], lk.k[kb + 1], U[j].y);
+        mac32(A[cs], lk.k[kb + 2], U[j].z);
+        mac32(A[cs], lk.k[kb + 3], U[j].w);
+      }
+      part[0] = A[0];
+      part[1] = A[1];
+    }
+    // ---- combine the 8 lanes of each group, reduce, fold into level 2 ----
+#pragma unroll
+    for (int cs = 0; cs < CPG; cs++) {
+      Acc x = part[cs];
+#pragma unroll
+      for (int m = 1; m < 8; m <<= 1) {
+        Acc y = acc_shfl_xor(x, m);
+        acc_add(x, y);
+      }
+      const uint64_t c = c0 + (uint64_t)g * CPG + cs;
+      acc_add_word(x, b1);                      // Eq. (1): b_1 + sum a s
+      const Fe v1 = acc_reduce(x);
+      if (c == cb) res.v1_first = v1;
+      if (c < ce) acc_mac_fe(res.acc2, a2[c & 127], v1);
+    }
+  }
+  // sum the four groups' level-2 accumulators
+#pragma unroll
+  for (int m = 8; m < 32; m <<= 1) {
+    Acc y = acc_shfl_xor(res.acc2, m);
+    acc_add(res.acc2, y);
+  }
+  res.v1_first = fe_shfl(res.v1_first, 0);
+  return res;
+}
+
+// Level sizes of Algorithm 1 for a string of T words: T_0 = T, T_j = ceil(T_{j-1}/128).
+// L_eff = number of f_j applications (0 when T == 1).
+struct Geom {
+  uint64_t T[kL + 1];
+  int leff;
+};
+PMP_HDI Geom make_geom(uint64_t Twords) {
+  Geom gm;
+  gm.T[0] = Twords;
+  gm.leff = 0;
+  uint64_t t = Twords;
+  for (int j = 1; j <= (int)kL; j++) {
+    if (t > 1) {
+      t = (t + 127) / 128;
+      gm.leff = j;
+    }
+    gm.T[j] = t;
+  }
+  return gm;
+}
+
+// ============================================================= k_wstring
+// Warp per string from the work list (big strings first).  Nodes of level 2 are
+// produced in order; levels >= 3 are evaluated on the fly by lane 0 with the
+// bounded-memory streaming scheme of P:451-453 (one pending accumulator per level).
+template <int BITS>
+__global__ void __launch_bounds__(kWWarps * 32)
+k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
+          const uint64_t *__restrict__ offsets, uint64_t n, void *__restrict__ out,
+          const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
+  using T = Tr<BITS>;
+  using Acc = typename T::Acc;
+  using Fe = typename T::Fe;
+  const int lane = threadIdx.x & 31;
+  const uint64_t *bk = keys;           // b_1..b_8
+  const uint64_t *ak = keys + kL;      // a_{j,i} at ak[(j-1)*128 + i]
+  LaneKeys<BITS> lk;
+  lk.load(ak, lane & 7);
+  const uint32_t nmid = wcount[0], nbig = wcount[1];
+  const uint32_t total = nmid + nbig;
+  for (;;) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(&wcount[2], 1u);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= total) break;
+    const uint64_t i = item < nbig ? wlist[n - 1 - item] : wlist[item - nbig];
+    const uint64_t o0 = offsets[i], o1 = offsets[i + 1];
+    StrView s;
+    s.base = bytes + o0;
+    s.g0 = 0;
+    s.B = o1 - o0;
+    s.avail_end = s.B;
+    s.delta = (uint32_t)((uintptr_t)s.base & 15);
+    const Geom gm = make_geom(s.B / T::W + 1);
+    Fe root;
+    if (gm.leff == 1) {                               // one level-1 block
+      root = warp_chunks<BITS>(s, 0, 1, lk, bk[0], ak + kM, lane).v1_first;
+    } else {
+      // streaming upper levels: pending sums for levels 3..8 (lane 0 only)
+      Acc up[kL - 2];
+      uint64_t pushed[kL - 2];
+#pragma unroll
+      for (int j = 0; j < (int)kL - 2; j++) {
+        acc_zero(up[j]);
+        pushed[j] = 0;
+      }
+      for (uint64_t q = 0; q < gm.T[2]; q++) {
+        const uint64_t cb = q * 128, ce = min(cb + 128, gm.T[1]);
+        ChunkOut<BITS> co = warp_chunks<BITS>(s, cb, ce, lk, bk[0], ak + kM, lane);
+        acc_add_word(co.acc2, bk[1]);                 // b_2
+        Fe v = acc_reduce(co.acc2);                   // v_{2,q}
+        if (gm.leff == 2) {
+          root = v;
+        } else if (lane == 0) {
+          // push v into level 3, carrying completed nodes upward
+          for (int j = 3; j <= gm.leff; j++) {
+            const int li = j - 3;
+            acc_mac_fe(up[li], ak[(uint64_t)(j - 1) * kM + (pushed[li] & 127)], v);
+            pushed[li]++;
+            if ((pushed[li] & 127) != 0 && pushed[li] != gm.T[j - 1]) break;  // node still open
+            acc_add_word(up[li], bk[j - 1]);
+            v = acc_reduce(up[li]);
+            acc_zero(up[li]);
+            if (j == gm.leff) root = v;
+          }
+        }
+      }
+    }
+    if (lane == 0) store_digest<BITS>(out, i, fe_lo(root));
+  }
+}
+
+// ============================================================= long string
+// Partial tree of one long string split across callers (ranks): every level-1
+// chunk value v_1 includes b_1; every level >= 2 sums a_{j,r} * child over the
+// children the caller owns, without b_j.  The key-only constant C (all v_1 = 0)
+// is added once in k_combine, so V = C + sum over callers ("Long
+// strings: affine split").
+template <int BITS>
+__global__ void __launch_bounds__(kWWarps * 32)
+k_node(const uint64_t *__restrict__ keys, StrView s, uint64_t cb, uint64_t ce, uint64_t qb, uint64_t qe,
+       int single, uint64_t *__restrict__ s2) {
+  using T = Tr<BITS>;
+  using Fe = typename T::Fe;
+  const int lane = threadIdx.x & 31;
+  const uint64_t *bk = keys, *ak = keys + kL;
+  const uint64_t warp = (uint64_t)blockIdx.x * kWWarps + (threadIdx.x >> 5);
+  const uint64_t nw = (uint64_t)gridDim.x * kWWarps;
+  if (single) {  // whole tree is one level-1 block (or no block at all)
+    if (warp != 0) return;
+    if (s.B < (uint64_t)T::W) {  // T == 1: the sole value is sigma_0 (reading Q2)
+      if (lane == 0) {
+        uint64_t w = 0;
+        for (uint32_t k = 0; k < (uint32_t)s.B; k++) w |= (uint64_t)s.base[k] << (8 * k);
+        w |= 1ULL << (8 * s.B);
+        Fe v = fe_from_word(w, (Fe *)nullptr);
+        fe_store(s2, v);
+      }
+      return;
+    }
+    LaneKeys<BITS> lk;
+    lk.load(ak, lane & 7);
+    ChunkOut<BITS> co = warp_chunks<BITS>(s, 0, 1, lk, bk[0], ak + kM, lane);
+    if (lane == 0) fe_store(s2, co.v1_first);
+    return;
+  }
+  if (warp >= qe - qb) return;
+  LaneKeys<BITS> lk;
+  lk.load(ak, lane & 7);
+  for (uint64_t q = qb + warp; q < qe; q += nw) {
+    const uint64_t lo = max(q * 128, cb), hi = min(q * 128 + 128, ce);
+    ChunkOut<BITS> co = warp_chunks<BITS>(s, lo, hi, lk, bk[0], ak + kM, lane);
+    const Fe v = acc_reduce(co.acc2);
+    if (lane == 0) fe_store(s2 + 2 * (q - qb), v);
+  }
+}
+
+// out node q (global index) = sum over owned children c in [128q, 128q+128) of
+// a_{j, c mod 128} * in[c - in_lo]; children are field elements (lo, hi).
+template <int BITS>
+__global__ void __launch_bounds__(kWWarps * 32)
+k_level(const uint64_t *__restrict__ keys, int j, const uint64_t *__restrict__ in, uint64_t in_lo,
+        uint64_t in_cnt, uint64_t *__restrict__ outv, uint64_t out_lo, uint64_t out_cnt) {
+  using T = Tr<BITS>;
+  using Acc = typename T::Acc;
+  using Fe = typename T::Fe;
+  const int lane = threadIdx.x & 31;
+  const uint64_t *aj = keys + kL + (uint64_t)(j - 1) * kM;
+  const uint64_t warp = (uint64_t)blockIdx.x * kWWarps + (threadIdx.x >> 5);
+  const uint64_t nw = (uint64_t)gridDim.x * kWWarps;
+  for (uint64_t qi = warp; qi < out_cnt; qi += nw) {
+    const uint64_t q = out_lo + qi;
+    Acc x;
+    acc_zero(x);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint64_t c = q * 128 + lane + 32 * k;
+      if (c >= in_lo && c < in_lo + in_cnt) {
+        Fe v;
+        fe_load(in + 2 * (c - in_lo), v);
+        acc_mac_fe(x, aj[lane + 32 * k], v);
+      }
+    }
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      Acc y = acc_shfl_xor(x, m);
+      acc_add(x, y);
+    }
+    if (lane == 0) fe_store(outv + 2 * qi, acc_reduce(x));
+  }
+}
+
+// V = C + sum_g P_g mod p; digest = mix(V mod 2^n)
+template <int BITS>
+__global__ void k_combine(const uint64_t *__restrict__ partials, int G, uint64_t c_lo, uint64_t c_hi,
+                          void *__restrict__ out) {
+  using T = Tr<BITS>;
+  using Acc = typename T::Acc;
+  using Fe = typename T::Fe;
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Acc x;
+  acc_zero(x);
+  uint64_t cw[2] = {c_lo, c_hi};
+  Fe c;
+  fe_load(cw, c);
+  acc_add_fe(x, c);
+  for (int g = 0; g < G; g++) {
+    Fe v;
+    fe_load(partials + 2 * g, v);
+    acc_add_fe(x, v);
+  }
+  store_digest<BITS>(out, 0, fe_lo(acc_reduce(x)));
+}
+
+// ============================================================= self-test hooks
+// mode 0: reduce the exact value (w0 + w1 2^n + w2 2^2n) mod p through the
+//         3->2 reduction + Algorithm 2; in = 3 words, out = (lo, hi).
+// mode 1: one block f(s) = (b + sum a_i s_i) mod p with the hot-loop MAC;
+//         in = [b, a_0..a_127, s_0..s_127], out = (lo, hi).
+// mode 2: out = mix(in[0]).
+template <int BITS>
+__global__ void k_selftest(int mode, const uint64_t *__restrict__ in, uint64_t n, uint64_t *__restrict__ outv) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  if (mode == 0) {
+    const uint64_t *w = in + 3 * t;
+    if constexpr (BITS == 64) {
+      Acc5 x = {(uint32_t)w[0], (uint32_t)(w[0] >> 32), (uint32_t)w[1], (uint32_t)(w[1] >> 32), (uint32_t)w[2]};
+      fe_store(outv + 2 * t, reduce_acc5(x));
+    } else {
+      Acc3 x = {(uint32_t)w[0], (uint32_t)w[1], (uint32_t)w[2]};
+      fe_store(outv + 2 * t, reduce_acc3(x));
+    }
+  } else if (mode == 1) {
+    const uint64_t *blk = in + 257 * t;
+    if constexpr (BITS == 64) {
+      MacAcc64 A;
+      macc_zero(A);
+      for (int i = 0; i < 128; i++) mac64(A, blk[1 + i], blk[129 + i]);
+      Acc5 x = macc_normalize(A);
+      acc5_add_u64(x, blk[0]);
+      fe_store(outv + 2 * t, reduce_acc5(x));
+    } else {
+      Acc3 A = {0, 0, 0};
+      for (int i = 0; i < 128; i++) mac32(A, (uint32_t)blk[1 + i], (uint32_t)blk[129 + i]);
+      acc3_add_u64(A, blk[0]);
+      fe_store(outv + 2 * t, reduce_acc3(A));
+    }
+  } else {
+    outv[2 * t] = BITS == 64 ? mix64(in[t]) : mix32((uint32_t)in[t]);
+    outv[2 * t + 1] = 0;
+  }
+}
+
+}  // namespace pmp

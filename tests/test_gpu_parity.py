@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, bit-exact.
+
+Integer hashing has exactly one correct digest per input, so every
+comparison is element-by-element equality.  Sizes span several 4 KiB warp
+tiles, level-2 nodes (128 blocks) and ragged tails; alignment offsets 0..15 are
+swept for the realignment path.
+"""
+import os
+import random
+
+import numpy as np
+import pytest
+
+import datagen
+import paper_1609_09840_b200 as pmp
+
+pytestmark = pytest.mark.gpu
+NT = os.cpu_count() or 4
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+
+    import __graft_entry__
+
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+    return torch.device("cuda:0")
+
+
+def _u(bits):
+    return np.uint64 if bits == 64 else np.uint32
+
+
+def run_batch(torch_dev, keys, payload: np.ndarray, offsets: np.ndarray):
+    import torch
+
+    d_pay = torch.from_numpy(np.ascontiguousarray(payload) if payload.size else np.zeros(16, np.uint8)).to(torch_dev)
+    d_off = torch.from_numpy(np.ascontiguousarray(offsets).view(np.int64)).to(torch_dev)
+    out = pmp.hash_batch(keys, d_pay, d_off)
+    torch.cuda.synchronize()
+    return pmp.as_u64(out)
+
+
+def oracle_batch(oracle_lib, seed, bits, payload, offsets):
+    ok = oracle_lib.keygen(seed, bits)
+    return oracle_lib.hash_batch(ok, payload, offsets, nthreads=NT).astype(_u(bits))
+
+
+# ------------------------------------------------------------ device arithmetic
+@pytest.mark.parametrize("bits", [32, 64])
+def test_reduction_fuzz_and_algorithm2_branches(torch_dev, oracle_lib, bits):
+    """Section 6.2 + Algorithm 2 on the device vs the exact residue mod p.
+    Random 3-word values with w2 <= 128 plus constructed witnesses that
+    reach every Algorithm 2 branch, including v1 = 2 (reading Q6), which random
+    inputs never reach."""
+    import torch
+
+    n_bits = bits
+    p = oracle_lib.params(bits)["p"]
+    k = p - 2**bits
+    mask = 2**n_bits - 1
+    rng = random.Random(bits)
+    cases = []
+    for _ in range(200_000):
+        cases.append((rng.getrandbits(n_bits), rng.getrandbits(n_bits), rng.randrange(0, 129)))
+    # witnesses: v1 = 2 branch (w0 = 2^n - j), v1 = 1 branch (0,1,0), boundary battery
+    for j in range(1, 2 * k + 3):
+        cases.append(((2**n_bits - j) & mask, 0, 0))
+    cases += [(0, 1, 0), (0, 0, 0), (k - 1, 0, 0), (2 * k - 1, 2, 0), (mask, mask, 128),
+              (30, 2, 0), (k, 0, 0), (p & mask, p >> n_bits, 0), ((p - 1) & mask, (p - 1) >> n_bits, 0)]
+    arr = np.array(cases, dtype=np.uint64)
+    d_in = torch.from_numpy(arr.view(np.int64)).to(torch_dev)
+    d_out = torch.zeros(2 * len(cases), dtype=torch.int64, device=torch_dev)
+    rc = pmp.pmp_selftest(bits, 0, d_in.data_ptr(), len(cases), d_out.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    out = d_out.cpu().numpy().view(np.uint64).reshape(-1, 2)
+    for (w0, w1, w2), (lo, hi) in zip(cases, out):
+        val = int(w0) + (int(w1) << n_bits) + (int(w2) << (2 * n_bits))
+        got = int(lo) + (int(hi) << 64) if bits == 64 else int(lo)
+        assert got == val % p, (w0, w1, w2)
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_block_mac_matches_oracle(torch_dev, oracle_lib, bits):
+    """The hot-loop multiply-accumulate + reduction on full 128-word blocks,
+    including maximal keys and words, vs the oracle's Eq. (1)."""
+    import torch
+
+    pr = oracle_lib.params(bits)
+    rng = np.random.default_rng(bits)
+    n = 3000
+    recs = np.zeros((n, 257), dtype=np.uint64)
+    hi = 2**bits - 1
+    recs[:, 0] = rng.integers(0, hi, size=n, dtype=np.uint64, endpoint=True)
+    recs[:, 1:129] = rng.integers(1, pr["a_max"], size=(n, 128), dtype=np.uint64, endpoint=True)
+    recs[:, 129:] = rng.integers(0, hi, size=(n, 128), dtype=np.uint64, endpoint=True)
+    recs[0, 0], recs[0, 1:129], recs[0, 129:] = hi, pr["a_max"], hi  # S:73 maximal case
+    recs[1, 129:] = 0
+    d_in = torch.from_numpy(recs.reshape(-1).view(np.int64)).to(torch_dev)
+    d_out = torch.zeros(2 * n, dtype=torch.int64, device=torch_dev)
+    assert pmp.pmp_selftest(bits, 1, d_in.data_ptr(), n, d_out.data_ptr(),
+                            torch.cuda.current_stream().cuda_stream) == 0
+    out = d_out.cpu().numpy().view(np.uint64).reshape(-1, 2)
+    for t in range(n):
+        want = oracle_lib.block(pr["p"], 128, int(recs[t, 0]), recs[t, 1:129], recs[t, 129:])
+        assert int(out[t, 0]) + (int(out[t, 1]) << 64) == want, t
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_mixer_matches_oracle(torch_dev, oracle_lib, bits):
+    import torch
+
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, 2**bits - 1, size=10000, dtype=np.uint64, endpoint=True)
+    x[:3] = [0, 1, 2**bits - 1]
+    d_in = torch.from_numpy(x.view(np.int64)).to(torch_dev)
+    d_out = torch.zeros(2 * x.size, dtype=torch.int64, device=torch_dev)
+    assert pmp.pmp_selftest(bits, 2, d_in.data_ptr(), x.size, d_out.data_ptr(),
+                            torch.cuda.current_stream().cuda_stream) == 0
+    out = d_out.cpu().numpy().view(np.uint64).reshape(-1, 2)[:, 0]
+    assert all(int(o) == oracle_lib.mix(bits, int(v)) for o, v in zip(out, x))
+
+
+# ------------------------------------------------------------ batch path
+@pytest.mark.parametrize("bits", [32, 64])
+def test_tiny_config_every_hash(torch_dev, oracle_lib, bits):
+    """configs[0] (1,000 strings, U[1,64] B, seed 1), every digest; at 32 bits too."""
+    wl = datagen.WORKLOADS["tiny"]
+    lens = wl.lengths()
+    off = datagen.offsets_from_lengths(lens)
+    pay = datagen.payload_host(wl.seed, 0, int(off[-1]))
+    keys = pmp.Keys.generate(wl.seed, bits)
+    got = run_batch(torch_dev, keys, pay, off)
+    want = oracle_batch(oracle_lib, wl.seed, bits, pay, off)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+@pytest.mark.parametrize("shift", [0, 1, 3, 8, 13])
+def test_length_sweep_all_paths(torch_dev, oracle_lib, bits, shift):
+    """Every length 0..2100 (short path <= 127 B, warp path beyond, 1..3 level-1
+    blocks, ragged tails, marker-only blocks), payload shifted by `shift` bytes."""
+    lens = np.arange(0, 2101, dtype=np.uint64)
+    rng = np.random.default_rng(shift)
+    rng.shuffle(lens)
+    off = datagen.offsets_from_lengths(lens) + shift
+    pay = datagen.payload_host(11 + shift, 0, int(off[-1]))
+    keys = pmp.Keys.generate(11, bits)
+    got = run_batch(torch_dev, keys, pay, off)
+    want = oracle_batch(oracle_lib, 11, bits, pay, off)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, [(int(i), int(lens[i])) for i in bad[:10]]
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_all_short_batch_alignments(torch_dev, oracle_lib, bits):
+    """The staged all-short warp path with every start alignment and empty strings."""
+    rng = np.random.default_rng(bits + 100)
+    lens = rng.integers(0, 128, size=20000, dtype=np.uint64)
+    lens[::17] = 0
+    off = datagen.offsets_from_lengths(lens) + 5
+    pay = datagen.payload_host(3, 0, int(off[-1]))
+    keys = pmp.Keys.generate(3, bits)
+    assert np.array_equal(run_batch(torch_dev, keys, pay, off), oracle_batch(oracle_lib, 3, bits, pay, off))
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_long_strings_in_batch(torch_dev, oracle_lib, bits):
+    """Warp-per-string path across level-2 (128 blocks) and level-3 (128^2 blocks)
+    boundaries, misaligned starts, mixed with short strings and big ones first."""
+    cb = 128 * bits // 8
+    lens = [cb * 128 - 1, cb * 128, cb * 128 + 1, cb * 128 * 2 + 5, 300_000, 70_000, 5, 0, 127, 128,
+            cb * 128 * 128 + cb + 3, 3 * cb, 3 * cb + 1]
+    lens = np.array(lens, dtype=np.uint64)
+    off = datagen.offsets_from_lengths(lens) + 7
+    pay = datagen.payload_host(21, 0, int(off[-1]))
+    keys = pmp.Keys.generate(21, bits)
+    got = run_batch(torch_dev, keys, pay, off)
+    want = oracle_batch(oracle_lib, 21, bits, pay, off)
+    assert np.array_equal(got, want), np.nonzero(got != want)[0]
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_algorithm2_rare_branches_end_to_end(torch_dev, oracle_lib, bits):
+    """Key schedules built so a block sum equals 2^n - j (v1 = 2 branch of
+    Algorithm 2) or 2^n (v1 = 1 branch): b = 2^n - 2 - j, a = 1, one data word 1
+    and the marker word 1 -> S = b + 1 + 1."""
+    import torch
+
+    w = bits // 8
+    for j in [0, 1, 5, 12, 13, 14, 15, 16, 29, 30, 31]:
+        bval = (2**bits - 2 - j) % 2**bits
+        b = np.full(8, bval, dtype=np.uint64)
+        a = np.ones((8, 128), dtype=np.uint64)
+        keys = pmp.Keys.from_words(bits, b, a)
+        data = (1).to_bytes(w, "little")
+        pay = np.frombuffer(data * 3 + b"\x00" * 13, dtype=np.uint8).copy()
+        off = np.array([0, w, 2 * w, 3 * w], dtype=np.uint64)
+        got = run_batch(torch_dev, keys, pay, off)
+        ok = oracle_lib.Keys(bits, b, a)
+        want = oracle_lib.hash_batch(ok, pay, off).astype(_u(bits))
+        assert np.array_equal(got, want), j
+        d = torch.from_numpy(pay[:w].copy()).to(torch_dev)
+        assert int(pmp.as_u64(pmp.hash_long(keys, d, w))[0]) == int(want[0])
+
+
+# ------------------------------------------------------------ long path
+LONG_LENS = [0, 1, 7, 8, 9, 1000, 1023, 1024, 1025, 4096, 128 * 1024 - 8, 128 * 1024, 128 * 1024 + 1,
+             128 * 512, 128 * 512 + 3, 1 << 20, (1 << 20) + 13, 128 * 128 * 1024 + 1024 + 9,
+             128 * 128 * 1024, 128 * 128 * 512 - 4]
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_hash_long_lengths(torch_dev, oracle_lib, bits):
+    import torch
+
+    ok = oracle_lib.keygen(4, bits)
+    keys = pmp.Keys.generate(4, bits)
+    big = datagen.payload_host(4, 0, max(LONG_LENS) + 64)
+    d_big = torch.from_numpy(big).to(torch_dev)
+    for L in LONG_LENS:
+        for shift in (0, 5):
+            got = int(pmp.as_u64(pmp.hash_long(keys, d_big[shift:], L))[0])
+            want = oracle_lib.hash_long(ok, big[shift:shift + L], nthreads=NT)
+            assert got == want, (L, shift)
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_long_partition_invariance(torch_dev, oracle_lib, bits):
+    """Partial + combine over G block-aligned ranges gives the same digest as
+    one call, for G = 1..8 and random splits (SURVEY 8(c.3) partition invariance)."""
+    import torch
+
+    cb = 128 * bits // 8
+    total = 3 * 128 * 128 * cb // 2 + 777  # three level-3 subtrees' worth, ragged
+    keys = pmp.Keys.generate(8, bits)
+    data = datagen.payload_host(8, 0, total)
+    d = torch.from_numpy(data).to(torch_dev)
+    ref = int(pmp.as_u64(pmp.hash_long(keys, d, total))[0])
+    want = oracle_lib.hash_long(oracle_lib.keygen(8, bits), data, nthreads=NT)
+    assert ref == want
+    rng = random.Random(bits)
+    splits = [pmp.pmp_long_split(bits, total, G) for G in (1, 2, 3, 4, 8)]
+    for _ in range(4):
+        cuts = sorted(rng.sample(range(1, total // cb), 5))
+        splits.append([0] + [c * cb for c in cuts] + [total])
+    for b in splits:
+        G = len(b) - 1
+        parts = torch.zeros(2 * G, dtype=torch.int64, device=torch_dev)
+        for g in range(G):
+            pmp.hash_long_partial(keys, d[b[g]:], b[g + 1] - b[g], b[g], total, partial=parts[2 * g:2 * g + 2])
+        got = int(pmp.as_u64(pmp.hash_long_combine(keys, parts, total))[0])
+        assert got == ref, b
