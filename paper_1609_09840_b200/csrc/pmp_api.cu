@@ -346,22 +346,37 @@ int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offs
   if (!bytes || !offsets || !out || n >= (1ULL << 32)) return PMP_EINVAL;
   if (int rc = check_keys(k)) return rc;
   const int sms = sm_count(k->device);
-  Scratch sc(st);
+  Scratch sc(st), sc_off(st);
   // work list (n u32) + counters [mid, big, next]
   if (sc.alloc((size_t)n * 4 + 16)) return PMP_ENOMEM;
   uint32_t *wcount = (uint32_t *)sc.p;
   uint32_t *wlist = wcount + 4;
   if (cudaMemsetAsync(wcount, 0, 16, st) != cudaSuccess) return PMP_ECUDA;
   const ParamKeys pk = param_keys(k);
-  const uint64_t warps = (n + 31) / 32;
-  uint64_t grid = (warps + kShortWarps - 1) / kShortWarps;
-  const uint64_t maxgrid = (uint64_t)sms * 6;  // resident blocks (33 KB smem each)
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    cudaFuncSetAttribute(k_short<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
+    cudaFuncSetAttribute(k_short<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
+  });
+  // the offsets ring is fed by TMA bulk copies, which need 16-byte aligned sources
+  if ((uintptr_t)offsets & 15) {
+    void *al = nullptr;
+    if (cudaMallocAsync(&al, (size_t)(n + 1) * 8, st) != cudaSuccess) return PMP_ENOMEM;
+    if (cudaMemcpyAsync(al, offsets, (size_t)(n + 1) * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return PMP_ECUDA;
+    sc_off.p = al;
+    offsets = (const uint64_t *)al;
+  }
+  uint64_t grid = (n + kTile - 1) / kTile;
+  const uint64_t per_sm = (228u * 1024u) / (kShortSmem + 1024u);  // resident blocks per SM (smem bound)
+  const uint64_t maxgrid = (uint64_t)sms * (per_sm ? per_sm : 1);  // persistent grid
   if (grid > maxgrid) grid = maxgrid;
+  const int threads = (kShortWarps + 1) * 32;  // + producer warp
   int rc;
   if (k->bits == 64)
-    rc = launch("k_short", st, [&] { k_short<64><<<(unsigned)grid, kShortWarps * 32, 0, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
+    rc = launch("k_short", st, [&] { k_short<64><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
   else
-    rc = launch("k_short", st, [&] { k_short<32><<<(unsigned)grid, kShortWarps * 32, 0, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
+    rc = launch("k_short", st, [&] { k_short<32><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
   if (rc) return rc;
   const unsigned wgrid = (unsigned)sms * 8;  // persistent, work list drained by atomics
   if (k->bits == 64)

@@ -55,50 +55,68 @@ struct Acc5 {        // exact value c0 + c1 2^32 + ... + c4 2^128
   uint32_t c0, c1, c2, c3, c4;
 };
 
-struct MacAcc64 {    // carry-save: (L1:L0) + cL 2^64 + ((M1:M0) + cM 2^64) 2^32 + ((H1:H0) + cH 2^64) 2^64
-  uint32_t L0, L1, cL, M0, M1, cM, H0, H1, cH;
+struct MacAcc64 {    // carry-save: L + cL 2^64 + (M + cM 2^64 + N + cN 2^64) 2^32 + (H + cH 2^64) 2^64
+  uint64_t L, M, N, H;  // 64-bit so each product lands in an aligned register pair (one IMAD.WIDE.U32)
+  uint32_t cL, cM, cN, cH;
 };
 
 PMP_DI void macc_zero(MacAcc64 &A) {
-  A.L0 = A.L1 = A.cL = A.M0 = A.M1 = A.cM = A.H0 = A.H1 = A.cH = 0;
+  A.L = A.M = A.N = A.H = 0;
+  A.cL = A.cM = A.cN = A.cH = 0;
 }
 
-// A += a * s  (a, s < 2^64).  Two SASS ops per 32x32 partial product.
+// A += a * s  (a, s < 2^64).  One IMAD.WIDE.U32 (carry out) per 32x32 partial
+// product plus carry-counter updates (IADD3.X / IMAD.X); the four partial
+// products go to four independent accumulators (no serial dependence inside a word).
 PMP_DI void mac64(MacAcc64 &A, uint32_t a0, uint32_t a1, uint32_t s0, uint32_t s1) {
-  asm("mad.lo.cc.u32  %0, %9, %11, %0;\n\t"
-      "madc.hi.cc.u32 %1, %9, %11, %1;\n\t"
-      "addc.u32       %2, %2, 0;\n\t"
-      "mad.lo.cc.u32  %3, %9, %12, %3;\n\t"
-      "madc.hi.cc.u32 %4, %9, %12, %4;\n\t"
+  asm("{\n\t.reg .u32 l0, l1, m0, m1, n0, n1, h0, h1;\n\t"
+      "mov.b64 {l0, l1}, %0;\n\t"
+      "mov.b64 {m0, m1}, %1;\n\t"
+      "mov.b64 {n0, n1}, %2;\n\t"
+      "mov.b64 {h0, h1}, %3;\n\t"
+      "mad.lo.cc.u32  l0, %8, %10, l0;\n\t"
+      "madc.hi.cc.u32 l1, %8, %10, l1;\n\t"
+      "addc.u32       %4, %4, 0;\n\t"
+      "mad.lo.cc.u32  m0, %8, %11, m0;\n\t"
+      "madc.hi.cc.u32 m1, %8, %11, m1;\n\t"
       "addc.u32       %5, %5, 0;\n\t"
-      "mad.lo.cc.u32  %3, %10, %11, %3;\n\t"
-      "madc.hi.cc.u32 %4, %10, %11, %4;\n\t"
-      "addc.u32       %5, %5, 0;\n\t"
-      "mad.lo.cc.u32  %6, %10, %12, %6;\n\t"
-      "madc.hi.cc.u32 %7, %10, %12, %7;\n\t"
-      "addc.u32       %8, %8, 0;"
-      : "+r"(A.L0), "+r"(A.L1), "+r"(A.cL), "+r"(A.M0), "+r"(A.M1), "+r"(A.cM),
-        "+r"(A.H0), "+r"(A.H1), "+r"(A.cH)
+      "mad.lo.cc.u32  n0, %9, %10, n0;\n\t"
+      "madc.hi.cc.u32 n1, %9, %10, n1;\n\t"
+      "addc.u32       %6, %6, 0;\n\t"
+      "mad.lo.cc.u32  h0, %9, %11, h0;\n\t"
+      "madc.hi.cc.u32 h1, %9, %11, h1;\n\t"
+      "addc.u32       %7, %7, 0;\n\t"
+      "mov.b64 %0, {l0, l1};\n\t"
+      "mov.b64 %1, {m0, m1};\n\t"
+      "mov.b64 %2, {n0, n1};\n\t"
+      "mov.b64 %3, {h0, h1};\n\t}"
+      : "+l"(A.L), "+l"(A.M), "+l"(A.N), "+l"(A.H), "+r"(A.cL), "+r"(A.cM), "+r"(A.cN), "+r"(A.cH)
       : "r"(a0), "r"(a1), "r"(s0), "r"(s1));
 }
 PMP_DI void mac64(MacAcc64 &A, uint64_t a, uint64_t s) {
   mac64(A, (uint32_t)a, (uint32_t)(a >> 32), (uint32_t)s, (uint32_t)(s >> 32));
 }
 
-// carry-save -> exact limbs (value unchanged)
+// carry-save -> exact limbs (value unchanged):
+//   S = L + (M + N) 2^32 + H 2^64 + cL 2^64 + (cM + cN) 2^96 + cH 2^128
 PMP_DI Acc5 macc_normalize(const MacAcc64 &A) {
   Acc5 r;
-  r.c0 = A.L0;
+  r.c0 = (uint32_t)A.L;
   asm("add.cc.u32  %0, %5, %6;\n\t"     // c1 = L1 + M0
       "addc.cc.u32 %1, %7, %8;\n\t"     // c2 = M1 + H0 + cy
       "addc.cc.u32 %2, %9, %10;\n\t"    // c3 = H1 + cM + cy
       "addc.u32    %3, %11, 0;\n\t"     // c4 = cH + cy
       "add.cc.u32  %1, %1, %4;\n\t"     // c2 += cL
       "addc.cc.u32 %2, %2, 0;\n\t"
+      "addc.u32    %3, %3, 0;\n\t"
+      "add.cc.u32  %0, %0, %12;\n\t"    // c1 += N0
+      "addc.cc.u32 %1, %1, %13;\n\t"    // c2 += N1 + cy
+      "addc.cc.u32 %2, %2, %14;\n\t"    // c3 += cN + cy
       "addc.u32    %3, %3, 0;"
       : "=r"(r.c1), "=r"(r.c2), "=r"(r.c3), "=r"(r.c4)
-      : "r"(A.cL), "r"(A.L1), "r"(A.M0), "r"(A.M1), "r"(A.H0), "r"(A.H1), "r"(A.cM),
-        "r"(A.cH));
+      : "r"(A.cL), "r"((uint32_t)(A.L >> 32)), "r"((uint32_t)A.M), "r"((uint32_t)(A.M >> 32)),
+        "r"((uint32_t)A.H), "r"((uint32_t)(A.H >> 32)), "r"(A.cM), "r"(A.cH),
+        "r"((uint32_t)A.N), "r"((uint32_t)(A.N >> 32)), "r"(A.cN));
   return r;
 }
 

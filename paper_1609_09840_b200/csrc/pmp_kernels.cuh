@@ -23,8 +23,7 @@ namespace pmp {
 
 constexpr uint32_t kShortMax = 127;      // bytes; k_short handles B <= kShortMax
 constexpr uint32_t kBigBytes = 1u << 16; // work-list class "big" (processed first)
-constexpr int kShortWarps = 8;           // warps per k_short block
-constexpr int kStageUnits = 264;         // 16-byte units of staging per warp (>= 32*127+15+132 bytes)
+constexpr int kShortWarps = 12;          // consumer warps per k_short block (+1 producer)
 constexpr int kWWarps = 4;               // warps per k_wstring / k_node block
 constexpr uint32_t FULL = 0xffffffffu;
 
@@ -49,6 +48,11 @@ PMP_DI uint32_t ld_u32(const void *p) {
   return r;
 }
 PMP_DI uint32_t funnel(uint32_t lo, uint32_t hi, uint32_t sh) { return __funnelshift_r(lo, hi, sh); }
+PMP_DI uint32_t lds_u32(uint32_t saddr) {
+  uint32_t r;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(saddr));
+  return r;
+}
 
 // ------------------------------------------------------------- width traits
 template <int BITS> struct Tr;
@@ -114,77 +118,252 @@ template <> PMP_DI void store_digest<32>(void *out, uint64_t i, uint64_t lo) {
 // ============================================================= k_short
 // One short string (B <= kShortMax, so T = floor(B/w)+1 <= 16 / 32 words and
 // the tree is a single f_1 block, or no block at all when T == 1).
-// `p` points at the aligned 32-bit word containing the first byte, `sh` is the
-// bit offset of that byte; words are read with `fetch(k)` (4-byte units).
+// fetch(k) returns the k-th aligned 32-bit word of the region starting at the
+// word containing the string's first byte; `sh` is that byte's bit offset.
+// The loop runs to the warp's largest number of full words; a lane past its
+// own full words multiplies zeros (a*0 adds nothing), so the multiply-adds are
+// never branched around.  The marker word is done once per lane with
+// its key read from shared memory.
 template <int BITS, class Fetch>
-PMP_DI uint64_t short_tree_lo(const ParamKeys &K, uint32_t B, uint32_t sh, int tmax, Fetch fetch) {
+PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ skeys, uint32_t B, uint32_t sh,
+                              int tfull_max, Fetch fetch) {
   if constexpr (BITS == 64) {
-    const uint32_t tlast = B >> 3, r = B & 7;                 // word T-1 holds the marker
-    const uint64_t lmask = (1ULL << (8 * r)) - 1, marker = 1ULL << (8 * r);
+    const int tlast = (int)(B >> 3);
+    const uint32_t r = B & 7;
     MacAcc64 A;
     macc_zero(A);
-    uint64_t sigma0 = 0;
     uint32_t y0 = fetch(0);
 #pragma unroll
-    for (int t = 0; t < 16; t++) {
-      if (t > tmax) break;
-      uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
-      uint64_t w = ((uint64_t)funnel(y1, y2, sh) << 32) | funnel(y0, y1, sh);
-      y0 = y2;
-      if (t == (int)tlast) w = (w & lmask) | marker;
-      if (t == 0) sigma0 = w;
-      if (t <= (int)tlast) mac64(A, K.a[t], w);                // Eq. (1), lazy
+    for (int tb = 0; tb < 16; tb += 4) {
+      if (tb >= tfull_max) break;                              // warp-uniform, once per 4 words
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int t = tb + j;
+        if (t >= 15) break;                                    // compile-time
+        const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
+        uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
+        y0 = y2;
+        if ((uint32_t)t >= (uint32_t)tlast) lo = hi = 0;       // past this lane's full words
+        mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lo, hi);  // Eq. (1), lazy
+      }
     }
-    if (tlast == 0) return sigma0;                             // |sigma| = 1: no f_j (reading Q2)
+    const uint32_t z0 = fetch(2 * tlast), z1 = fetch(2 * tlast + 1), z2 = fetch(2 * tlast + 2);
+    uint64_t w = ((uint64_t)funnel(z1, z2, sh) << 32) | funnel(z0, z1, sh);
+    w = (w & ((1ULL << (8 * r)) - 1)) | (1ULL << (8 * r));    // bytes || 0x01 || 0
+    if (tlast == 0) return w;                                  // |sigma| = 1: no f_j (reading Q2)
+    mac64(A, skeys[tlast], w);
     Acc5 x = macc_normalize(A);
     acc5_add_u64(x, K.b);
     return reduce_acc5(x).lo;                                  // mod p, then mod 2^64
   } else {
-    const uint32_t tlast = B >> 2, r = B & 3;
-    const uint32_t lmask = (1u << (8 * r)) - 1, marker = 1u << (8 * r);
+    const int tlast = (int)(B >> 2);
+    const uint32_t r = B & 3;
     Acc3 A = {0, 0, 0};
-    uint32_t sigma0 = 0;
     uint32_t y0 = fetch(0);
 #pragma unroll
-    for (int t = 0; t < 32; t++) {
-      if (t > tmax) break;
-      uint32_t y1 = fetch(t + 1);
-      uint32_t w = funnel(y0, y1, sh);
-      y0 = y1;
-      if (t == (int)tlast) w = (w & lmask) | marker;
-      if (t == 0) sigma0 = w;
-      if (t <= (int)tlast) mac32(A, (uint32_t)K.a[t], w);
+    for (int tb = 0; tb < 32; tb += 8) {
+      if (tb >= tfull_max) break;                              // warp-uniform, once per 8 words
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int t = tb + j;
+        if (t >= 31) break;
+        const uint32_t y1 = fetch(t + 1);
+        uint32_t w = funnel(y0, y1, sh);
+        y0 = y1;
+        if ((uint32_t)t >= (uint32_t)tlast) w = 0;
+        mac32(A, (uint32_t)K.a[t], w);
+      }
     }
-    if (tlast == 0) return sigma0;
+    const uint32_t z0 = fetch(tlast), z1 = fetch(tlast + 1);
+    uint32_t w = funnel(z0, z1, sh);
+    w = (w & ((1u << (8 * r)) - 1)) | (1u << (8 * r));
+    if (tlast == 0) return w;
+    mac32(A, (uint32_t)skeys[tlast], w);
     acc3_add_u64(A, K.b);
     return (uint32_t)reduce_acc3(A);
   }
 }
 
+// ---- TMA bulk-copy / mbarrier helpers (cp.async.bulk -> UBLKCP in SASS)
+PMP_DI uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+PMP_DI void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+PMP_DI void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+}
+PMP_DI void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+PMP_DI void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+PMP_DI void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "PMP_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra PMP_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+PMP_DI void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// k_short: warp-specialised TMA pipeline.  A block = 1 producer warp + kShortWarps
+// consumer warps, working on tiles of kTile = 32 * kShortWarps consecutive
+// strings (grid-strided).  Shared memory holds
+//   - an offsets ring (kRing slots): the kTile+1 offsets of tile k, one TMA bulk
+//     copy issued kOffAhead tiles ahead;
+//   - a byte ring (kByteRing bytes): the 16-byte aligned contiguous byte span of
+//     each staged tile, one TMA bulk copy, packed back to back so the number of
+//     tiles in flight adapts to the string lengths;
+//   - a header per tile.
+// The producer's work per tile is O(1) (the span is [offsets[first],
+// offsets[last+1])), so one producer warp keeps many consumer warps fed.  A
+// tile whose span exceeds kSpanMaxTile is "direct": consumers read its short
+// strings from global.  Strings longer than kShortMax are appended by the
+// consumers to the work list of k_wstring in either mode.
+constexpr int kTile = 32 * kShortWarps;
+constexpr int kRing = 8, kOffAhead = 4;
+constexpr uint32_t kByteRing = 64 * 1024;
+constexpr uint32_t kSpanMaxTile = 32 * 1024;                   // larger spans go direct
+constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
+constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
+struct TileHdr {
+  uint64_t alo;    // global address of staged byte 0
+  uint32_t pos;    // ring position of staged byte 0
+  uint32_t mode;   // 0 staged, 1 direct
+};
+constexpr size_t kShortSmem = 256 /* keys */ + kByteRing + kSlack + 16 + (size_t)kRing * kOffBytes +
+                              (size_t)kRing * sizeof(TileHdr) +
+                              (size_t)(3 * kRing) * 8 + 128;
+
 template <int BITS>
-__global__ void __launch_bounds__(kShortWarps * 32)
+__global__ void __launch_bounds__((kShortWarps + 1) * 32)
 k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets,
         uint64_t n, void *__restrict__ out, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
-  __shared__ uint4 stage_all[kShortWarps][kStageUnits];
+  extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  uint4 *stage = stage_all[wib];
-  const uint32_t *stage32 = reinterpret_cast<const uint32_t *>(stage);
-  const uint64_t gstride = (uint64_t)gridDim.x * kShortWarps * 32;
-  for (uint64_t base = ((uint64_t)blockIdx.x * kShortWarps + wib) * 32; base < n; base += gstride) {
-    const uint64_t i = base + lane;
-    const bool valid = i < n;
-    uint64_t o0 = 0, o1 = 0;
-    if (valid) {
-      o0 = offsets[i];
-      o1 = offsets[i + 1];
+  uint64_t *skeys = reinterpret_cast<uint64_t *>(smem);                       // a_{1,0..31}
+  uint8_t *ring = smem + 256;                                                  // kByteRing (+ slack)
+  uint64_t *offs = reinterpret_cast<uint64_t *>(ring + kByteRing + kSlack + 16);  // kRing x kOffBytes
+  TileHdr *hdr = reinterpret_cast<TileHdr *>(reinterpret_cast<uint8_t *>(offs) + (size_t)kRing * kOffBytes);
+  uint64_t *bar_off = reinterpret_cast<uint64_t *>(hdr + kRing);  // offsets landed (producer)
+  uint64_t *bar_done = bar_off + kRing;                            // tile consumed (producer)
+  uint64_t *bar_full = bar_done + kRing;                           // tile ready (consumers)
+  if (threadIdx.x < 32) skeys[threadIdx.x] = K.a[threadIdx.x];
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kRing; q++) {
+      mbar_init(&bar_off[q], 1);
+      mbar_init(&bar_done[q], kShortWarps);
+      mbar_init(&bar_full[q], 1);
     }
-    const uint64_t B = o1 - o0;
-    const bool is_short = valid && B <= kShortMax;
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const uint32_t ntiles = (uint32_t)((n + kTile - 1) / kTile);
+  // tiles of this block: blockIdx.x + k * gridDim.x
+  const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto tile_base = [&](uint32_t k) { return ((uint64_t)blockIdx.x + (uint64_t)k * gridDim.x) * kTile; };
+  auto off_slot = [&](uint32_t k) { return offs + (size_t)(k & (kRing - 1)) * (kOffBytes / 8); };
+
+  if (wib == kShortWarps) {
+    // ------------------------------------------------------------ producer warp
+    auto wait_done = [&](uint32_t k) {  // tile k fully consumed
+      mbar_wait(&bar_done[k & (kRing - 1)], (k / kRing) & 1);
+    };
+    auto issue_offs = [&](uint32_t k) {
+      if (k >= kRing) wait_done(k - kRing);  // slot reuse
+      if (lane == 0) {
+        const int q = (int)(k & (kRing - 1));
+        const uint64_t base = tile_base(k);
+        const uint64_t cnt = min((uint64_t)kTile + 1, n + 1 - base);
+        const uint32_t nb = (uint32_t)((cnt * 8 + 15) & ~15ULL);
+        mbar_arrive_tx(&bar_off[q], nb);
+        bulk_g2s(off_slot(k), offsets + base, nb, &bar_off[q]);
+      }
+    };
+    // byte-ring bookkeeping (identical in every lane): [tail, head) is in use;
+    // tile k's bytes end at tend[k % kRing]; `oldest` is the first unreleased tile.
+    uint32_t head = 0, tail = 0, oldest = 0;
+    __shared__ uint32_t tend[kRing];
+    for (uint32_t k = 0; k < (uint32_t)kOffAhead && k < my_tiles; k++) issue_offs(k);
+    for (uint32_t k = 0; k < my_tiles; k++) {
+      const int q = (int)(k & (kRing - 1));
+      if (k + kOffAhead < my_tiles) issue_offs(k + kOffAhead);
+      mbar_wait(&bar_off[q], (k / kRing) & 1);
+      const uint64_t base = tile_base(k);
+      const uint32_t nv = (uint32_t)min((uint64_t)kTile, n - base);  // strings in this tile
+      const uint64_t *o = off_slot(k);
+      // span of the tile and its place in the byte ring
+      uint32_t mode = 1, nb = 0, pos = 0;
+      uintptr_t alo = 0;
+      {
+        const uint64_t first = o[0], endo = o[nv];
+        alo = (uintptr_t)(bytes + first) & ~(uintptr_t)15;
+        const uintptr_t ahi = ((uintptr_t)(bytes + endo) + 15) & ~(uintptr_t)15;
+        const uint64_t span = first < endo ? (uint64_t)(ahi - alo) : 0;
+        if (span <= kSpanMaxTile) {
+          mode = 0;
+          nb = (uint32_t)span;
+          uint32_t start = head;
+          if ((start % kByteRing) + nb > kByteRing) start += kByteRing - (start % kByteRing);  // no wrap inside a span
+          while (start + nb - tail > kByteRing) {  // release consumed tiles until the span fits
+            wait_done(oldest);
+            tail = tend[oldest & (kRing - 1)];
+            oldest++;
+          }
+          pos = start % kByteRing;
+          head = start + nb;
+        }
+      }
+      // keep `oldest` within kRing of k so tend[] slots are not overwritten early
+      while (k - oldest >= (uint32_t)kRing - 1) {
+        wait_done(oldest);
+        tail = tend[oldest & (kRing - 1)];
+        oldest++;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        tend[q] = head;
+        hdr[q].alo = (uint64_t)alo;
+        hdr[q].pos = pos;
+        hdr[q].mode = mode;
+        mbar_arrive_tx(&bar_full[q], nb);   // release: hdr and offsets visible to consumers
+        if (nb) bulk_g2s(ring + pos, reinterpret_cast<const void *>(alo), nb, &bar_full[q]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumer warps
+  const uint32_t ring_s = smem_u32(ring);
+  const uint64_t tstride = (uint64_t)gridDim.x * kTile;
+  uint64_t i = (uint64_t)blockIdx.x * kTile + 32 * wib + lane;
+  for (uint32_t k = 0; k < my_tiles; k++, i += tstride) {
+    const int q = (int)(k & (kRing - 1));
+    mbar_wait(&bar_full[q], (k / kRing) & 1);
+    const bool valid = i < n;
+    const uint32_t mode = hdr[q].mode;
+    const uint64_t *o = offs + (size_t)q * (kOffBytes / 8) + 32 * wib + lane;
+    uint64_t o0 = 0, Bl = 0;
+    if (valid) {
+      o0 = o[0];
+      Bl = o[1] - o0;
+    }
+    const bool is_short = valid && Bl <= kShortMax;
     const bool is_long = valid && !is_short;
+    const uint32_t B = (uint32_t)(is_short ? Bl : 0);
     const unsigned longmask = __ballot_sync(FULL, is_long);
     if (longmask) {
       // warp-aggregated append: big strings from the back, others from the front
-      const bool big = is_long && B >= kBigBytes;
+      const bool big = is_long && Bl >= kBigBytes;
       const unsigned bigmask = __ballot_sync(FULL, big), midmask = longmask & ~bigmask;
       uint32_t mbase = 0, bbase = 0;
       if (lane == 0) {
@@ -197,47 +376,28 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
       if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
       if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
     }
-    int tmax = 0;  // warp max of the marker word index
-    if (is_short) tmax = (int)(B / (BITS / 8));
-    tmax = (int)__reduce_max_sync(FULL, (unsigned)tmax);
-    uint64_t lo = 0;
-    if (longmask == 0) {
-      // all strings short: stage the warp's contiguous byte span [first, end)
-      const int last = 31 - __clz(__ballot_sync(FULL, valid));
-      const uint64_t first = __shfl_sync(FULL, o0, 0);
-      const uint64_t endo = __shfl_sync(FULL, o1, last);
-      const uintptr_t alo = (uintptr_t)(bytes + first) & ~(uintptr_t)15;
-      const uintptr_t ahi = ((uintptr_t)(bytes + endo) + 15) & ~(uintptr_t)15;
-      const int nunits = first < endo ? (int)((ahi - alo) >> 4) : 0;
-      uint4 tmp[9];
-#pragma unroll
-      for (int k = 0; k < 9; k++) {
-        const int u = lane + 32 * k;
-        if (u < nunits) tmp[k] = ld_stream16(reinterpret_cast<const void *>(alo + 16 * (uintptr_t)u));
+    // warp max of the number of full words (the marker word is handled apart)
+    const int tfm = (int)__reduce_max_sync(FULL, B / (BITS / 8));
+    if (is_short) {
+      uint64_t lo;
+      if (mode == 0) {
+        const uint32_t sofs = hdr[q].pos + (uint32_t)((uintptr_t)(bytes + o0) - (uintptr_t)hdr[q].alo);
+        const uint32_t pa = ring_s + (sofs & ~3u);
+        lo = short_tree_lo<BITS>(K, skeys, B, 8 * (sofs & 3), tfm, [&](int kk) { return lds_u32(pa + 4 * kk); });
+      } else {
+        // direct tile: read the string's aligned 32-bit words straight from global,
+        // touching only words that overlap [start, end) (never past offsets[n]).
+        const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
+        const uintptr_t pa = sa & ~(uintptr_t)3;
+        lo = short_tree_lo<BITS>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, [&](int kk) {
+          const uintptr_t a = pa + 4 * (uintptr_t)kk;
+          return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
+        });
       }
-#pragma unroll
-      for (int k = 0; k < 9; k++) {
-        const int u = lane + 32 * k;
-        if (u < nunits) stage[u] = tmp[k];
-      }
-      __syncwarp();
-      if (is_short) {
-        const uint32_t s = (uint32_t)((uintptr_t)(bytes + o0) - alo);
-        const uint32_t *p = stage32 + (s >> 2);
-        lo = short_tree_lo<BITS>(K, (uint32_t)B, 8 * (s & 3), tmax, [&](int k) { return p[k]; });
-      }
-      __syncwarp();
-    } else if (is_short) {
-      // mixed warp: read the string's aligned 32-bit words straight from global,
-      // touching only words that overlap [start, end) (never past offsets[n]).
-      const uintptr_t sa = (uintptr_t)(bytes + o0), se = (uintptr_t)(bytes + o1);
-      const uintptr_t pa = sa & ~(uintptr_t)3;
-      lo = short_tree_lo<BITS>(K, (uint32_t)B, 8 * (uint32_t)(sa & 3), tmax, [&](int k) {
-        const uintptr_t a = pa + 4 * (uintptr_t)k;
-        return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
-      });
+      store_digest<BITS>(out, i, lo);
     }
-    if (is_short) store_digest<BITS>(out, i, lo);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bar_done[q]);
   }
 }
 
@@ -469,10 +629,11 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   const int lane = threadIdx.x & 31;
   const uint64_t *bk = keys;           // b_1..b_8
   const uint64_t *ak = keys + kL;      // a_{j,i} at ak[(j-1)*128 + i]
-  LaneKeys<BITS> lk;
-  lk.load(ak, lane & 7);
   const uint32_t nmid = wcount[0], nbig = wcount[1];
   const uint32_t total = nmid + nbig;
+  if (total == 0) return;
+  LaneKeys<BITS> lk;
+  lk.load(ak, lane & 7);
   for (;;) {
     uint32_t item = 0;
     if (lane == 0) item = atomicAdd(&wcount[2], 1u);
