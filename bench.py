@@ -282,6 +282,7 @@ def main():
     launches = pmp.pmp_launch_count() - l0
     ms = ev0.elapsed_time(ev1)
     k_ms, k_cnt = pmp.pmp_prof_read(dominant)
+    kernel_ms = {name: pmp.pmp_prof_read(name) for name in ("k_short", "k_wstring", "k_node", "k_level", "k_combine")}
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -323,6 +324,7 @@ def main():
                          "launches_timed": k_cnt},
             "clocks": clocks,
             "gpu_launches": launches,
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kernel_ms.items() if v[1]},
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

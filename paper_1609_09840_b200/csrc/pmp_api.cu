@@ -97,6 +97,13 @@ int sm_count(int dev) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     g_dev[dev].sms = v > 0 ? v : 148;
+    // keep stream-ordered scratch cached in the device's default pool instead
+    // of returning it to the OS at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     g_dev[dev].init = true;
   }
   return g_dev[dev].sms;
@@ -378,7 +385,7 @@ int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offs
   else
     rc = launch("k_short", st, [&] { k_short<32><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
   if (rc) return rc;
-  const unsigned wgrid = (unsigned)sms * 8;  // persistent, work list drained by atomics
+  const unsigned wgrid = (unsigned)sms * 4;  // persistent, work list drained by atomics
   if (k->bits == 64)
     rc = launch("k_wstring", st, [&] { k_wstring<64><<<wgrid, kWWarps * 32, 0, st>>>(k->d_blob, bytes, offsets, n, out, wlist, wcount); });
   else

@@ -229,7 +229,8 @@ PMP_DI void mbar_arrive(uint64_t *bar) {
 // tile whose span exceeds kSpanMaxTile is "direct": consumers read its short
 // strings from global.  Strings longer than kShortMax are appended by the
 // consumers to the work list of k_wstring in either mode.
-constexpr int kTile = 32 * kShortWarps;
+constexpr int kPasses = 1;                                     // strings per consumer lane per tile
+constexpr int kTile = 32 * kShortWarps * kPasses;              // 384
 constexpr int kRing = 8, kOffAhead = 4;
 constexpr uint32_t kByteRing = 64 * 1024;
 constexpr uint32_t kSpanMaxTile = 32 * 1024;                   // larger spans go direct
@@ -345,56 +346,63 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   // -------------------------------------------------------------- consumer warps
   const uint32_t ring_s = smem_u32(ring);
   const uint64_t tstride = (uint64_t)gridDim.x * kTile;
-  uint64_t i = (uint64_t)blockIdx.x * kTile + 32 * wib + lane;
+  uint64_t i = (uint64_t)blockIdx.x * kTile + 32 * wib + lane;  // (tile base + lane slot)
   for (uint32_t k = 0; k < my_tiles; k++, i += tstride) {
     const int q = (int)(k & (kRing - 1));
     mbar_wait(&bar_full[q], (k / kRing) & 1);
-    const bool valid = i < n;
     const uint32_t mode = hdr[q].mode;
-    const uint64_t *o = offs + (size_t)q * (kOffBytes / 8) + 32 * wib + lane;
-    uint64_t o0 = 0, Bl = 0;
-    if (valid) {
-      o0 = o[0];
-      Bl = o[1] - o0;
-    }
-    const bool is_short = valid && Bl <= kShortMax;
-    const bool is_long = valid && !is_short;
-    const uint32_t B = (uint32_t)(is_short ? Bl : 0);
-    const unsigned longmask = __ballot_sync(FULL, is_long);
-    if (longmask) {
-      // warp-aggregated append: big strings from the back, others from the front
-      const bool big = is_long && Bl >= kBigBytes;
-      const unsigned bigmask = __ballot_sync(FULL, big), midmask = longmask & ~bigmask;
-      uint32_t mbase = 0, bbase = 0;
-      if (lane == 0) {
-        if (midmask) mbase = atomicAdd(&wcount[0], (uint32_t)__popc(midmask));
-        if (bigmask) bbase = atomicAdd(&wcount[1], (uint32_t)__popc(bigmask));
+    const uint32_t rpos = hdr[q].pos;
+    const uintptr_t ralo = (uintptr_t)hdr[q].alo;
+#pragma unroll 1
+    for (int pass = 0; pass < kPasses; pass++) {
+      const uint32_t jj = 32 * (wib * kPasses + pass) + lane;  // 32 consecutive strings per pass
+      const uint64_t ii = i - (32 * wib + lane) + jj;
+      const bool valid = ii < n;
+      const uint64_t *o = offs + (size_t)q * (kOffBytes / 8) + jj;
+      uint64_t o0 = 0, Bl = 0;
+      if (valid) {
+        o0 = o[0];
+        Bl = o[1] - o0;
       }
-      mbase = __shfl_sync(FULL, mbase, 0);
-      bbase = __shfl_sync(FULL, bbase, 0);
-      const unsigned lt = (1u << lane) - 1;
-      if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
-      if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
-    }
-    // warp max of the number of full words (the marker word is handled apart)
-    const int tfm = (int)__reduce_max_sync(FULL, B / (BITS / 8));
-    if (is_short) {
-      uint64_t lo;
-      if (mode == 0) {
-        const uint32_t sofs = hdr[q].pos + (uint32_t)((uintptr_t)(bytes + o0) - (uintptr_t)hdr[q].alo);
-        const uint32_t pa = ring_s + (sofs & ~3u);
-        lo = short_tree_lo<BITS>(K, skeys, B, 8 * (sofs & 3), tfm, [&](int kk) { return lds_u32(pa + 4 * kk); });
-      } else {
-        // direct tile: read the string's aligned 32-bit words straight from global,
-        // touching only words that overlap [start, end) (never past offsets[n]).
-        const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
-        const uintptr_t pa = sa & ~(uintptr_t)3;
-        lo = short_tree_lo<BITS>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, [&](int kk) {
-          const uintptr_t a = pa + 4 * (uintptr_t)kk;
-          return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
-        });
+      const bool is_short = valid && Bl <= kShortMax;
+      const bool is_long = valid && !is_short;
+      const uint32_t B = (uint32_t)(is_short ? Bl : 0);
+      const unsigned longmask = __ballot_sync(FULL, is_long);
+      if (longmask) {
+        // warp-aggregated append: big strings from the back, others from the front
+        const bool big = is_long && Bl >= kBigBytes;
+        const unsigned bigmask = __ballot_sync(FULL, big), midmask = longmask & ~bigmask;
+        uint32_t mbase = 0, bbase = 0;
+        if (lane == 0) {
+          if (midmask) mbase = atomicAdd(&wcount[0], (uint32_t)__popc(midmask));
+          if (bigmask) bbase = atomicAdd(&wcount[1], (uint32_t)__popc(bigmask));
+        }
+        mbase = __shfl_sync(FULL, mbase, 0);
+        bbase = __shfl_sync(FULL, bbase, 0);
+        const unsigned lt = (1u << lane) - 1;
+        if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)ii;
+        if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)ii;
       }
-      store_digest<BITS>(out, i, lo);
+      // warp max of the number of full words (the marker word is handled apart)
+      const int tfm = (int)__reduce_max_sync(FULL, B / (BITS / 8));
+      if (is_short) {
+        uint64_t lo;
+        if (mode == 0) {
+          const uint32_t sofs = rpos + (uint32_t)((uintptr_t)(bytes + o0) - ralo);
+          const uint32_t pa = ring_s + (sofs & ~3u);
+          lo = short_tree_lo<BITS>(K, skeys, B, 8 * (sofs & 3), tfm, [&](int kk) { return lds_u32(pa + 4 * kk); });
+        } else {
+          // direct tile: read the string's aligned 32-bit words straight from global,
+          // touching only words that overlap [start, end) (never past offsets[n]).
+          const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
+          const uintptr_t pa = sa & ~(uintptr_t)3;
+          lo = short_tree_lo<BITS>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, [&](int kk) {
+            const uintptr_t a = pa + 4 * (uintptr_t)kk;
+            return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
+          });
+        }
+        store_digest<BITS>(out, ii, lo);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&bar_done[q]);
