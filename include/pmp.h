@@ -127,7 +127,9 @@ int pmp_long_constant(const pmp_keys *keys, uint64_t total_len, uint64_t *c2);
  *         Section 6.2 reduction and Algorithm 2; w2 <= 2^16;
  * mode 1: in = n records [b, a_0..a_127, s_0..s_127] -> Eq. (1) via the
  *         hot-loop multiply-accumulate;
- * mode 2: in = n words -> mix_n(word).
+ * mode 2: in = n words -> mix_n(word);
+ * mode 3: as mode 0 but returns only (value mod p) mod 2^n, the folded
+ *         form the digest path uses.
  * in/out (device); out gets 2 uint64 per record (lo, hi). */
 int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_t *out,
                  struct CUstream_st *stream);

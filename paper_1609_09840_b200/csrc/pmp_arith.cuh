@@ -201,6 +201,32 @@ PMP_HDI Fe64 alg2_64(uint64_t v0, uint32_t v1) {
   return z;
 }
 
+// V mod 2^64 only (the digest input), same arithmetic as Section 6.2 +
+// Algorithm 2 with the branches folded:
+//   v = (w0 - u0) + (k^2 w2 + k u1 + k) + 2^64, so with d = w0 - u0 (borrow bw)
+//   and e = d + t (carry ce): v0 = e, v1 = ce + 1 - bw;
+//   Alg. 2 (corrected) gives lo = v0 - k v1 + k [v0 < k v1]  (mod 2^64):
+//   case k v1 <= v0 -> v0 - k v1; case v1 = 1, v0 < k -> v0 (hi = 1);
+//   case v1 = 2, v0 < 2k -> v0 - k (mod 2^64, hi = [v0 >= k]).
+PMP_HDI uint64_t reduce_lo_words64(uint64_t w0, uint64_t w1, uint64_t w2) {
+#ifdef __CUDA_ARCH__
+  const uint64_t u1 = __umul64hi(w1, kK64);
+#else
+  const uint64_t u1 = (uint64_t)(((unsigned __int128)w1 * kK64) >> 64);
+#endif
+  const uint64_t u0 = w1 * kK64;
+  const uint64_t t = kK64 * kK64 * w2 + kK64 * u1 + kK64;
+  const uint64_t d = w0 - u0;
+  const uint64_t bw = w0 < u0;
+  const uint64_t e = d + t;
+  const uint64_t v1 = (uint64_t)(e < t) + 1 - bw;
+  const uint64_t kv = kK64 * v1;
+  return e - kv + (e < kv ? kK64 : 0);
+}
+PMP_HDI uint64_t reduce_lo_acc5(const Acc5 &x) {
+  return reduce_lo_words64(((uint64_t)x.c1 << 32) | x.c0, ((uint64_t)x.c3 << 32) | x.c2, x.c4);
+}
+
 PMP_HDI Fe64 reduce_acc5(const Acc5 &x) {
   uint64_t w0 = ((uint64_t)x.c1 << 32) | x.c0;
   uint64_t w1 = ((uint64_t)x.c3 << 32) | x.c2;
@@ -275,6 +301,16 @@ PMP_HDI uint64_t alg2_32(uint32_t v0, uint32_t v1) {  // Algorithm 2 (corrected)
   if (kK32 * v1 <= v0) return (uint64_t)v0 - kK32 * v1;
   if (v1 == 1) return (1ULL << 32) + v0;
   return (1ULL << 32) + v0 - kK32;
+}
+
+// V mod 2^32 only, the same folding for n = 32 in 64-bit arithmetic:
+//   v = w0 + k^2 w2 + k u1 + 2^32 + k - u0 (< 3 * 2^32), v0 = v mod 2^32, v1 = v >> 32,
+//   lo = v0 - k v1 + k [v0 < k v1]  (mod 2^32).
+PMP_HDI uint32_t reduce_lo_acc3(const Acc3 &x) {
+  const uint64_t u = (uint64_t)x.c1 * kK32;
+  const uint64_t v = (uint64_t)x.c0 + kK32 * kK32 * x.c2 + kK32 * (u >> 32) + (1ULL << 32) + kK32 - (uint32_t)u;
+  const uint32_t v0 = (uint32_t)v, kv = (uint32_t)(kK32 * (v >> 32));
+  return v0 - kv + (v0 < kv ? (uint32_t)kK32 : 0u);
 }
 
 PMP_HDI uint64_t reduce_acc3(const Acc3 &x) {

@@ -154,7 +154,7 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
     mac64(A, skeys[tlast], w);
     Acc5 x = macc_normalize(A);
     acc5_add_u64(x, K.b);
-    return reduce_acc5(x).lo;                                  // mod p, then mod 2^64
+    return reduce_lo_acc5(x);                                  // mod p, then mod 2^64
   } else {
     const int tlast = (int)(B >> 2);
     const uint32_t r = B & 3;
@@ -180,7 +180,7 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
     if (tlast == 0) return w;
     mac32(A, (uint32_t)skeys[tlast], w);
     acc3_add_u64(A, K.b);
-    return (uint32_t)reduce_acc3(A);
+    return reduce_lo_acc3(A);
   }
 }
 
@@ -802,6 +802,7 @@ __global__ void k_combine(const uint64_t *__restrict__ partials, int G, uint64_t
 // mode 1: one block f(s) = (b + sum a_i s_i) mod p with the hot-loop MAC;
 //         in = [b, a_0..a_127, s_0..s_127], out = (lo, hi).
 // mode 2: out = mix(in[0]).
+// mode 3: as mode 0 but only (value mod p) mod 2^n (the digest input).
 template <int BITS>
 __global__ void k_selftest(int mode, const uint64_t *__restrict__ in, uint64_t n, uint64_t *__restrict__ outv) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -830,6 +831,16 @@ __global__ void k_selftest(int mode, const uint64_t *__restrict__ in, uint64_t n
       acc3_add_u64(A, blk[0]);
       fe_store(outv + 2 * t, reduce_acc3(A));
     }
+  } else if (mode == 3) {
+    const uint64_t *w = in + 3 * t;
+    if constexpr (BITS == 64) {
+      Acc5 x = {(uint32_t)w[0], (uint32_t)(w[0] >> 32), (uint32_t)w[1], (uint32_t)(w[1] >> 32), (uint32_t)w[2]};
+      outv[2 * t] = reduce_lo_acc5(x);
+    } else {
+      Acc3 x = {(uint32_t)w[0], (uint32_t)w[1], (uint32_t)w[2]};
+      outv[2 * t] = reduce_lo_acc3(x);
+    }
+    outv[2 * t + 1] = 0;
   } else {
     outv[2 * t] = BITS == 64 ? mix64(in[t]) : mix32((uint32_t)in[t]);
     outv[2 * t + 1] = 0;
