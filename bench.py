@@ -94,15 +94,30 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- workloads
 def make_batch(wl, rank, n=None):
-    """Host lengths/offsets for this rank's batch (data seed differs per rank)."""
+    """Host lengths/offsets for this rank's batch.
+
+    hashtable/fixed4k/tiny: each rank hashes its own batch of the recipe (data
+    seed + 256*rank).  mixed (configs[4], ~295 GiB, sized for 8 GPUs): rank r
+    hashes byte-balanced shard r of 8 of the one global corpus; returns
+    offsets rebased to the shard and the shard's first payload byte."""
+    if wl.name == "mixed":
+        from paper_1609_09840_b200 import parallel
+
+        lens = wl.lengths()
+        offs_all = datagen.offsets_from_lengths(lens)
+        lo, hi = parallel.shard_batch(offs_all, 8)[rank % 8]
+        if n is not None:
+            hi = min(hi, lo + n)
+        sub, b0, _ = parallel.rebase_offsets(offs_all, lo, hi)
+        return wl.seed, lens[lo:hi], sub, b0
     n = wl.n if n is None else n
     seed = wl.seed + 256 * rank
     lens = datagen.lengths(wl.kind, seed, n, wl.lo, wl.hi)
     offs = datagen.offsets_from_lengths(lens)
-    return seed, lens, offs
+    return seed, lens, offs, 0
 
 
-def oracle_sample_rate(wl, seed, offs, bits_list, budget_s=12.0, max_threads=None):
+def oracle_sample_rate(wl, seed, offs, bits_list, budget_s=12.0, max_threads=None, base=0):
     """Oracle GB/s on a bounded prefix sample of the batch (all host threads)."""
     import oracle
 
@@ -110,13 +125,15 @@ def oracle_sample_rate(wl, seed, offs, bits_list, budget_s=12.0, max_threads=Non
     keys = {b: oracle.keygen(wl.seed, b) for b in bits_list}
     # calibrate on 2^15 strings, then size the sample to ~budget_s
     n_cal = min(1 << 15, offs.size - 1)
-    pay = datagen.payload_host(seed, 0, int(offs[n_cal]))
+    if wl.name == "mixed":
+        n_cal = min(1 << 9, offs.size - 1)
+    pay = datagen.payload_host(seed, base, int(offs[n_cal]))
     t0 = time.perf_counter()
     for b in bits_list:
         oracle.hash_batch(keys[b], pay, offs[:n_cal + 1], nthreads=threads)
     dt = time.perf_counter() - t0
     n_s = int(min(offs.size - 1, max(n_cal, n_cal * budget_s / max(dt, 1e-6))))
-    pay = datagen.payload_host(seed, 0, int(offs[n_s]))
+    pay = datagen.payload_host(seed, base, int(offs[n_s]))
     t0 = time.perf_counter()
     for b in bits_list:
         oracle.hash_batch(keys[b], pay, offs[:n_s + 1], nthreads=threads)
@@ -152,9 +169,9 @@ def run_reference(args, wl):
                 rates.append(r)
                 times.append(dt)
     else:
-        seed, lens, offs = make_batch(wl, 0, n=min(wl.n, 1 << 22))
+        seed, lens, offs, b0 = make_batch(wl, 0, n=min(wl.n, 1 << 22))
         for i in range(args.warmup + args.steps):
-            r, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=4.0)
+            r, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=4.0, base=b0)
             if i >= args.warmup:
                 rates.append(r)
                 times.append(dt)
@@ -171,7 +188,8 @@ def run_reference(args, wl):
 
 
 def workload_config(wl, gpus):
-    c = {"workload": wl.name, "strings_per_gpu": wl.n, "len_bytes": [wl.lo, wl.hi],
+    c = {"workload": wl.name, "strings_per_gpu": wl.n if wl.name != "mixed" else "shard of 8 (~2^19)",
+         "len_bytes": [wl.lo, wl.hi],
          "len_dist": {0: "fixed", 1: "uniform", 2: "log-uniform"}[wl.kind], "bits": list(wl.bits),
          "key_seed": wl.seed, "parallelism": f"dp{gpus}" if not wl.long else f"split{gpus}",
          "l2": "inputs larger than L2 (126 MB); no flush needed"}
@@ -243,11 +261,13 @@ def main():
         alg_bytes_per_launch = hi - lo
         n = 1
     else:
-        seed, lens, offs = make_batch(wl, rank)
-        n = wl.n
+        seed, lens, offs, b0 = make_batch(wl, rank)
+        n = lens.size
         total_bytes = int(offs[-1])
-        d_pay = torch.empty(total_bytes + 16, dtype=torch.uint8, device=dev)
-        datagen.fill_device(seed, d_pay.data_ptr(), total_bytes, sp)
+        lead = b0 % datagen.PAGE
+        d_buf = torch.empty(total_bytes + lead + 16, dtype=torch.uint8, device=dev)
+        datagen.fill_device(seed, d_buf.data_ptr(), total_bytes + lead, sp, start=b0 - lead)
+        d_pay = d_buf[lead:]
         d_off = torch.from_numpy(offs.view(np.int64)).to(dev)
         for b in wl.bits:
             outs[b] = torch.empty(n, dtype=torch.int64 if b == 64 else torch.int32, device=dev)
@@ -345,10 +365,10 @@ def run_e2e(args, wl, pmp, keys, dev, stream, rank, world):
 
     if wl.long:
         return None
-    seed, lens, offs = make_batch(wl, rank)
-    n = wl.n
+    seed, lens, offs, b0 = make_batch(wl, rank)
+    n = lens.size
     total = int(offs[-1])
-    h_pay = torch.from_numpy(datagen.payload_host(seed, 0, total)).pin_memory()
+    h_pay = torch.from_numpy(datagen.payload_host(seed, b0, total)).pin_memory()
     h_off = torch.from_numpy(offs.view(np.int64)).pin_memory()
     d_pay = torch.empty(total + 16, dtype=torch.uint8, device=dev)
     d_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
@@ -390,8 +410,8 @@ def cpu_baseline(wl):
         if wl.long:
             v, cores, desc, dt = oracle_long_rate(wl, 256 << 20)
         else:
-            seed, lens, offs = make_batch(wl, 0, n=min(wl.n, 1 << 23))
-            v, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=10.0)
+            seed, lens, offs, b0 = make_batch(wl, 0, n=min(wl.n, 1 << 23))
+            v, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=10.0, base=b0)
         return {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc,
                 "seconds": dt}
     except Exception as e:  # pragma: no cover

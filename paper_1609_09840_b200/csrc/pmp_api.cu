@@ -385,11 +385,17 @@ int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offs
   else
     rc = launch("k_short", st, [&] { k_short<32><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
   if (rc) return rc;
-  const unsigned wgrid = (unsigned)sms * 4;  // persistent, work list drained by atomics
+  static std::once_flag wattr_once;
+  std::call_once(wattr_once, [] {
+    cudaFuncSetAttribute(k_wstring<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+    cudaFuncSetAttribute(k_wstring<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+  });
+  const uint64_t wper_sm = (228u * 1024u) / (kWSmem + 1024u);
+  const unsigned wgrid = (unsigned)(sms * (wper_sm ? wper_sm : 1));  // persistent, work list drained by atomics
   if (k->bits == 64)
-    rc = launch("k_wstring", st, [&] { k_wstring<64><<<wgrid, kWWarps * 32, 0, st>>>(k->d_blob, bytes, offsets, n, out, wlist, wcount); });
+    rc = launch("k_wstring", st, [&] { k_wstring<64><<<wgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, out, wlist, wcount); });
   else
-    rc = launch("k_wstring", st, [&] { k_wstring<32><<<wgrid, kWWarps * 32, 0, st>>>(k->d_blob, bytes, offsets, n, out, wlist, wcount); });
+    rc = launch("k_wstring", st, [&] { k_wstring<32><<<wgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, out, wlist, wcount); });
   return rc;
 }
 

@@ -158,6 +158,26 @@ PMP_DI void acc5_mac_fe(Acc5 &x, uint64_t a, const Fe64 &v) {
         "r"((uint32_t)(phi >> 32)), "r"((uint32_t)ahi), "r"((uint32_t)(ahi >> 32)));
 }
 
+// x += a * (v0 + v1 2^64) for a 3->2-reduced value (v1 <= 2): any
+// representative of v_1 mod p gives the same next-level value, so Algorithm 2
+// is skipped for values that are only multiplied into the next level.
+PMP_DI void acc5_mac_v01(Acc5 &x, uint64_t a, uint64_t v0, uint32_t v1) {
+  const uint64_t plo = a * v0, phi = __umul64hi(a, v0);
+  const uint64_t q = a * v1;                           // a v1 mod 2^64
+  const uint32_t qh = v1 == 2 ? (uint32_t)(a >> 63) : 0u;
+  asm("add.cc.u32  %0, %0, %5;\n\t"
+      "addc.cc.u32 %1, %1, %6;\n\t"
+      "addc.cc.u32 %2, %2, %7;\n\t"
+      "addc.cc.u32 %3, %3, %8;\n\t"
+      "addc.u32    %4, %4, %11;\n\t"
+      "add.cc.u32  %2, %2, %9;\n\t"
+      "addc.cc.u32 %3, %3, %10;\n\t"
+      "addc.u32    %4, %4, 0;"
+      : "+r"(x.c0), "+r"(x.c1), "+r"(x.c2), "+r"(x.c3), "+r"(x.c4)
+      : "r"((uint32_t)plo), "r"((uint32_t)(plo >> 32)), "r"((uint32_t)phi), "r"((uint32_t)(phi >> 32)),
+        "r"((uint32_t)q), "r"((uint32_t)(q >> 32)), "r"(qh));
+}
+
 PMP_DI Acc5 acc5_shfl_xor(const Acc5 &x, int m) {
   Acc5 r;
   r.c0 = __shfl_xor_sync(0xffffffffu, x.c0, m);
@@ -276,6 +296,19 @@ PMP_DI void acc3_mac_fe(Acc3 &x, uint32_t a, uint64_t v) {
       "addc.u32    %2, %2, 0;"
       : "+r"(x.c0), "+r"(x.c1), "+r"(x.c2)
       : "r"((uint32_t)prod), "r"((uint32_t)(prod >> 32)), "r"(ahi));
+}
+
+// x += a * (v0 + v1 2^32), v1 <= 2 (see acc5_mac_v01)
+PMP_DI void acc3_mac_v01(Acc3 &x, uint32_t a, uint32_t v0, uint32_t v1) {
+  const uint64_t prod = (uint64_t)a * v0;
+  const uint64_t q = (uint64_t)a * v1;                 // < 2^34, weight 2^32
+  asm("add.cc.u32  %0, %0, %3;\n\t"
+      "addc.cc.u32 %1, %1, %4;\n\t"
+      "addc.u32    %2, %2, 0;\n\t"
+      "add.cc.u32  %1, %1, %5;\n\t"
+      "addc.u32    %2, %2, %6;"
+      : "+r"(x.c0), "+r"(x.c1), "+r"(x.c2)
+      : "r"((uint32_t)prod), "r"((uint32_t)(prod >> 32)), "r"((uint32_t)q), "r"((uint32_t)(q >> 32)));
 }
 
 PMP_DI Acc3 acc3_shfl_xor(const Acc3 &x, int m) {

@@ -107,6 +107,31 @@ PMP_DI uint64_t fe_shfl(uint64_t v, int lane) { return __shfl_sync(FULL, v, lane
 PMP_DI Fe64 fe_from_word(uint64_t w, Fe64 *) { Fe64 r; r.lo = w; r.hi = 0; return r; }
 PMP_DI uint64_t fe_from_word(uint64_t w, uint64_t *) { return w; }
 
+PMP_DI void load_acc(const uint32_t *w, Acc5 &x) { x.c0 = w[0]; x.c1 = w[1]; x.c2 = w[2]; x.c3 = w[3]; x.c4 = w[4]; }
+PMP_DI void load_acc(const uint32_t *w, Acc3 &x) { x.c0 = w[0]; x.c1 = w[1]; x.c2 = w[2]; }
+PMP_DI void store_acc(uint32_t *w, const Acc5 &x) { w[0] = x.c0; w[1] = x.c1; w[2] = x.c2; w[3] = x.c3; w[4] = x.c4; }
+PMP_DI void store_acc(uint32_t *w, const Acc3 &x) { w[0] = x.c0; w[1] = x.c1; w[2] = x.c2; }
+// chunk sum -> a_2-weighted contribution without Algorithm 2 (acc5/acc3_mac_v01)
+PMP_DI void acc_mac_partial(Acc5 &acc, uint64_t a, const Acc5 &x) {
+  uint64_t v0;
+  uint32_t v1;
+  reduce3to2_64(((uint64_t)x.c1 << 32) | x.c0, ((uint64_t)x.c3 << 32) | x.c2, x.c4, v0, v1);
+  acc5_mac_v01(acc, a, v0, v1);
+}
+PMP_DI void acc_mac_partial(Acc3 &acc, uint64_t a, const Acc3 &x) {
+  uint32_t v0, v1;
+  reduce3to2_32(x.c0, x.c1, x.c2, v0, v1);
+  acc3_mac_v01(acc, (uint32_t)a, v0, v1);
+}
+// levels of Algorithm 1 applied to T words: 0 if T == 1, else ceil(log_128 T)
+PMP_HDI int levels_of(uint64_t T) {
+#ifdef __CUDA_ARCH__
+  return T <= 1 ? 0 : (64 - __clzll((long long)(T - 1)) + 6) / 7;
+#else
+  return T <= 1 ? 0 : (64 - __builtin_clzll(T - 1) + 6) / 7;
+#endif
+}
+
 template <int BITS> PMP_DI void store_digest(void *out, uint64_t i, uint64_t lo);
 template <> PMP_DI void store_digest<64>(void *out, uint64_t i, uint64_t lo) {
   reinterpret_cast<uint64_t *>(out)[i] = mix64(lo);
@@ -232,7 +257,7 @@ PMP_DI void mbar_arrive(uint64_t *bar) {
 constexpr int kPasses = 1;                                     // strings per consumer lane per tile
 constexpr int kTile = 32 * kShortWarps * kPasses;              // 384
 constexpr int kRing = 8, kOffAhead = 4;
-constexpr uint32_t kByteRing = 64 * 1024;
+constexpr uint32_t kByteRing = 40 * 1024;
 constexpr uint32_t kSpanMaxTile = 32 * 1024;                   // larger spans go direct
 constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
 constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
@@ -623,74 +648,287 @@ PMP_HDI Geom make_geom(uint64_t Twords) {
 }
 
 // ============================================================= k_wstring
-// Warp per string from the work list (big strings first).  Nodes of level 2 are
-// produced in order; levels >= 3 are evaluated on the fly by lane 0 with the
-// bounded-memory streaming scheme of P:451-453 (one pending accumulator per level).
+// Warp per string from the work list (big strings first).  Each warp streams
+// its strings through a private shared-memory ring of 4 KiB tiles: lane 0
+// issues TMA bulk copies up to kWStages-1 tiles ahead, across string
+// boundaries (it prefetches the next work item while the current string is
+// being issued), and the warp hashes tile t while tiles t+1.. are in flight.
+// A tile is 4 level-1 blocks (PM+64) / 8 (PM+32) of one string; its copy
+// starts at the 16-byte aligned address at or below the string's byte 4096 t
+// and carries 16 bytes of overlap, so a misaligned string is realigned from
+// shared memory (5 x LDS.32 + funnel shifts per 16 bytes) without shuffles.
+// Level 2 is accumulated per lane group and closed every 128 blocks; levels
+// >= 3 are streamed by lane 0 (bounded memory).
+constexpr int kWTile = 4096;
+constexpr int kWStages = 4;
+constexpr int kWStageBytes = kWTile + 32;      // + 16 B overlap + 16 B read slack
+constexpr int kWBlockWarps = 4;
+struct WStack {      // lane 0's streaming state for levels 3..8
+  uint64_t T[kL + 1];
+  uint64_t pushed[kL - 2];
+  uint32_t up[kL - 2][5];
+};
+struct WHdr {
+  uint64_t i;        // string index
+  uint64_t B;        // string length
+  uint32_t tile;     // tile index within the string
+  uint32_t ntiles;
+  uint32_t delta;    // string start & 15
+  uint32_t pad;
+};
+constexpr size_t kWSmemPerWarp =
+    ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + 127) & ~(size_t)127;
+constexpr size_t kWSmem = 2048 /* a_2 keys, b */ + kWBlockWarps * kWSmemPerWarp;
+
 template <int BITS>
-__global__ void __launch_bounds__(kWWarps * 32)
+PMP_DI uint4 tile_unit(uint32_t stage_s, uint32_t delta, uint32_t off) {
+  if (delta == 0) {
+    uint4 u;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                 : "r"(stage_s + off));
+    return u;
+  }
+  const uint32_t a = stage_s + ((delta + off) & ~3u), sh = 8 * (delta & 3);
+  const uint32_t y0 = lds_u32(a), y1 = lds_u32(a + 4), y2 = lds_u32(a + 8), y3 = lds_u32(a + 12),
+                 y4 = lds_u32(a + 16);
+  return make_uint4(funnel(y0, y1, sh), funnel(y1, y2, sh), funnel(y2, y3, sh), funnel(y3, y4, sh));
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kWBlockWarps * 32)
 k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
           const uint64_t *__restrict__ offsets, uint64_t n, void *__restrict__ out,
           const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
   using T = Tr<BITS>;
   using Acc = typename T::Acc;
   using Fe = typename T::Fe;
-  const int lane = threadIdx.x & 31;
+  constexpr int CPG = T::CPG, CPI = 4 * CPG, W = T::W;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int g = lane >> 3, r = lane & 7;
+  uint64_t *s_a2 = reinterpret_cast<uint64_t *>(smem);   // a_{2,0..127}
+  uint64_t *s_b = s_a2 + kM;                              // b_1..b_8
+  uint8_t *wbase = smem + 2048 + (size_t)wib * kWSmemPerWarp;
+  uint8_t *stg = wbase;                                                   // kWStages x kWStageBytes
+  WHdr *hdr = reinterpret_cast<WHdr *>(wbase + (size_t)kWStages * kWStageBytes);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(hdr + kWStages);
+  WStack *stk = reinterpret_cast<WStack *>(bar + kWStages);
   const uint64_t *bk = keys;           // b_1..b_8
   const uint64_t *ak = keys + kL;      // a_{j,i} at ak[(j-1)*128 + i]
   const uint32_t nmid = wcount[0], nbig = wcount[1];
   const uint32_t total = nmid + nbig;
   if (total == 0) return;
+  for (int k = threadIdx.x; k < (int)kM; k += blockDim.x) s_a2[k] = ak[kM + k];
+  if (threadIdx.x < kL) s_b[threadIdx.x] = bk[threadIdx.x];
+  __syncthreads();
+  const uint64_t b1 = s_b[0], b2 = s_b[1], a10 = ak[0];
+  if (lane == 0) {
+    for (int q = 0; q < kWStages; q++) mbar_init(&bar[q], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
   LaneKeys<BITS> lk;
-  lk.load(ak, lane & 7);
-  for (;;) {
-    uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(&wcount[2], 1u);
-    item = __shfl_sync(FULL, item, 0);
-    if (item >= total) break;
-    const uint64_t i = item < nbig ? wlist[n - 1 - item] : wlist[item - nbig];
-    const uint64_t o0 = offsets[i], o1 = offsets[i + 1];
-    StrView s;
-    s.base = bytes + o0;
-    s.g0 = 0;
-    s.B = o1 - o0;
-    s.avail_end = s.B;
-    s.delta = (uint32_t)((uintptr_t)s.base & 15);
-    const Geom gm = make_geom(s.B / T::W + 1);
-    Fe root;
-    if (gm.leff == 1) {                               // one level-1 block
-      root = warp_chunks<BITS>(s, 0, 1, lk, bk[0], ak + kM, lane).v1_first;
-    } else {
-      // streaming upper levels: pending sums for levels 3..8 (lane 0 only)
-      Acc up[kL - 2];
-      uint64_t pushed[kL - 2];
-#pragma unroll
-      for (int j = 0; j < (int)kL - 2; j++) {
-        acc_zero(up[j]);
-        pushed[j] = 0;
+  lk.load(ak, r);
+  const uint32_t stg_s = smem_u32(stg);
+
+  // ---- producer state (lane 0).  Work items are strided statically over the
+  // warps (item k of this warp = gw + k * nw over [big..., mid...]); lane 0
+  // keeps a two-deep metadata pipeline: the list entry of item k+2 and the
+  // offsets of item k+1 are in flight while item k's tiles are issued.
+  const uint32_t gw = blockIdx.x * kWBlockWarps + wib, nw = gridDim.x * kWBlockWarps;
+  auto list_at = [&](uint32_t item) -> uint64_t {
+    return item < nbig ? wlist[n - 1 - item] : wlist[item - nbig];
+  };
+  uint64_t p_i = 0, p_B = 0, p_nbytes = 0;
+  uintptr_t p_A = 0;
+  uint32_t p_tile = 0, p_ntiles = 0, p_delta = 0;
+  bool p_have = false;
+  uint32_t nx_item = gw;                     // next item to start issuing
+  uint64_t nx_i = 0, nx_o0 = 0, nx_o1 = 0;   // its metadata (valid if nx_item < total)
+  uint64_t nn_i = 0;                         // list entry of item nx_item + nw
+  if (lane == 0) {
+    if (nx_item < total) {
+      nx_i = list_at(nx_item);
+      nx_o0 = offsets[nx_i];
+      nx_o1 = offsets[nx_i + 1];
+    }
+    if (nx_item + nw < total) nn_i = list_at(nx_item + nw);
+  }
+  uint32_t issued = 0, consumed = 0;
+  auto produce = [&]() {  // lane 0: fill free ring slots
+    while (issued - consumed < (uint32_t)kWStages) {
+      if (!p_have || p_tile == p_ntiles) {
+        if (nx_item >= total) return;
+        p_i = nx_i;
+        p_B = nx_o1 - nx_o0;
+        const uintptr_t sa = (uintptr_t)(bytes + nx_o0);
+        p_A = sa & ~(uintptr_t)15;
+        p_delta = (uint32_t)(sa & 15);
+        p_nbytes = (((uintptr_t)(bytes + nx_o1) + 15) & ~(uintptr_t)15) - p_A;
+        const uint64_t T1 = (p_B / W + 1 + 127) / 128;           // level-1 blocks
+        p_ntiles = (uint32_t)((T1 + CPI - 1) / CPI);
+        p_tile = 0;
+        p_have = true;
+        // advance the metadata pipeline by one item
+        nx_item += nw;
+        if (nx_item < total) {
+          nx_i = nn_i;
+          nx_o0 = offsets[nx_i];
+          nx_o1 = offsets[nx_i + 1];
+        }
+        if (nx_item + nw < total) nn_i = list_at(nx_item + nw);
       }
-      for (uint64_t q = 0; q < gm.T[2]; q++) {
-        const uint64_t cb = q * 128, ce = min(cb + 128, gm.T[1]);
-        ChunkOut<BITS> co = warp_chunks<BITS>(s, cb, ce, lk, bk[0], ak + kM, lane);
-        acc_add_word(co.acc2, bk[1]);                 // b_2
-        Fe v = acc_reduce(co.acc2);                   // v_{2,q}
-        if (gm.leff == 2) {
-          root = v;
-        } else if (lane == 0) {
-          // push v into level 3, carrying completed nodes upward
-          for (int j = 3; j <= gm.leff; j++) {
-            const int li = j - 3;
-            acc_mac_fe(up[li], ak[(uint64_t)(j - 1) * kM + (pushed[li] & 127)], v);
-            pushed[li]++;
-            if ((pushed[li] & 127) != 0 && pushed[li] != gm.T[j - 1]) break;  // node still open
-            acc_add_word(up[li], bk[j - 1]);
-            v = acc_reduce(up[li]);
-            acc_zero(up[li]);
-            if (j == gm.leff) root = v;
-          }
+      const int q = (int)(issued % kWStages);
+      const uint64_t off = (uint64_t)p_tile * kWTile;
+      const uint32_t nb = off < p_nbytes ? (uint32_t)min((uint64_t)(kWTile + 16), p_nbytes - off) : 0u;
+      hdr[q].i = p_i;
+      hdr[q].B = p_B;
+      hdr[q].tile = p_tile;
+      hdr[q].ntiles = p_ntiles;
+      hdr[q].delta = p_delta;
+      hdr[q].pad = nb;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the slot
+      mbar_arrive_tx(&bar[q], nb);
+      if (nb) bulk_g2s(stg + (size_t)q * kWStageBytes, reinterpret_cast<const void *>(p_A + off), nb, &bar[q]);
+      p_tile++;
+      issued++;
+    }
+  };
+  if (lane == 0) produce();
+  issued = __shfl_sync(FULL, issued, 0);
+
+  // ---- consumer state (whole warp): the string being hashed
+  uint64_t tlast = 0, T1 = 0;
+  uint32_t rbytes = 0;
+  int leff = 0;
+  Acc acc2;
+  acc_zero(acc2);
+  Fe root = Fe();
+  while (consumed < issued) {
+    const int q = (int)(consumed % kWStages);
+    mbar_wait(&bar[q], (consumed / kWStages) & 1);
+    const uint64_t si = hdr[q].i;
+    const uint32_t t = hdr[q].tile, ntiles = hdr[q].ntiles, delta = hdr[q].delta;
+    const bool nodata = hdr[q].pad == 0;            // only the marker word (= 1) at word 128*c0
+    if (t == 0) {                                   // a new string starts
+      const uint64_t B = hdr[q].B;
+      tlast = B / W;
+      rbytes = (uint32_t)(B % W);
+      T1 = (tlast + 1 + 127) / 128;
+      leff = levels_of(tlast + 1);
+      acc_zero(acc2);
+      if (leff >= 3 && lane == 0) {                 // streaming state for levels >= 3
+        const Geom gm = make_geom(tlast + 1);
+        for (int j = 0; j <= (int)kL; j++) stk->T[j] = gm.T[j];
+        for (int j = 0; j < (int)kL - 2; j++) {
+          stk->pushed[j] = 0;
+          for (int l = 0; l < 5; l++) stk->up[j][l] = 0;
         }
       }
     }
-    if (lane == 0) store_digest<BITS>(out, i, fe_lo(root));
+    const uint32_t st_s = stg_s + (uint32_t)q * kWStageBytes;
+    const uint64_t c0 = (uint64_t)t * CPI;          // first level-1 block of this tile
+    uint4 U[8];
+    if (!nodata) {
+#pragma unroll
+      for (int j = 0; j < 8; j++) U[j] = tile_unit<BITS>(st_s, delta, 1024 * g + 16 * (r + 8 * j));
+      if (tlast < (c0 + CPI) * 128) {               // warp-uniform: the tile holds the marker word
+        const uint64_t tw0 = (c0 + (uint64_t)g * CPG) * 128;
+#pragma unroll
+        for (int j = 0; j < 8; j++) fixup_unit<BITS>(U[j], tw0 + (uint64_t)(16 * (r + 8 * j)) / W, tlast, rbytes);
+      }
+    }
+    // ---- level-1 multiply-accumulate (the hot loop) ----
+    Acc part[CPG];
+    if (nodata) {
+      // sigma of block c0 is (1, 0, ..., 0): its sum is a_{1,0} (added in lane 0 of group 0)
+#pragma unroll
+      for (int cs = 0; cs < CPG; cs++) {
+        acc_zero(part[cs]);
+        if (lane == 0 && cs == 0) acc_add_word(part[cs], a10);
+      }
+    } else if constexpr (BITS == 64) {
+      MacAcc64 A;
+      macc_zero(A);
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        mac64(A, (uint32_t)lk.k[2 * j], (uint32_t)(lk.k[2 * j] >> 32), U[j].x, U[j].y);
+        mac64(A, (uint32_t)lk.k[2 * j + 1], (uint32_t)(lk.k[2 * j + 1] >> 32), U[j].z, U[j].w);
+      }
+      part[0] = macc_normalize(A);
+    } else {
+      Acc3 A[2] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int cs = j >> 2, kb = 4 * (j & 3);
+        mac32(A[cs], lk.k[kb + 0], U[j].x);
+        mac32(A[cs], lk.k[kb + 1], U[j].y);
+        mac32(A[cs], lk.k[kb + 2], U[j].z);
+        mac32(A[cs], lk.k[kb + 3], U[j].w);
+      }
+      part[0] = A[0];
+      part[CPG - 1] = A[1];
+    }
+    __syncwarp();
+    // the slot is free: let lane 0 refill the ring before the reductions
+    consumed++;
+    if (lane == 0) produce();
+    issued = __shfl_sync(FULL, issued, 0);
+    // ---- combine the 8 lanes of each group, fold into level 2 ----
+#pragma unroll
+    for (int cs = 0; cs < CPG; cs++) {
+      Acc x = part[cs];
+#pragma unroll
+      for (int m = 1; m < 8; m <<= 1) {
+        Acc y = acc_shfl_xor(x, m);
+        acc_add(x, y);
+      }
+      const uint64_t c = c0 + (uint64_t)g * CPG + cs;
+      acc_add_word(x, b1);                          // Eq. (1): b_1 + sum a s
+      if (leff == 1) {
+        if (c == 0) root = acc_reduce(x);           // the whole tree is one block
+      } else if (c < T1) {
+        acc_mac_partial(acc2, s_a2[c & 127], x);    // a_{2, c mod 128} * v_1(c), v_1 3->2-reduced
+      }
+    }
+    // ---- close a level-2 node every 128 blocks and at the end of the string
+    const uint64_t cend = c0 + CPI;
+    if (leff >= 2 && ((cend & 127) == 0 || cend >= T1)) {
+      Acc x = acc2;
+#pragma unroll
+      for (int m = 8; m < 32; m <<= 1) {
+        Acc y = acc_shfl_xor(x, m);
+        acc_add(x, y);
+      }
+      acc_zero(acc2);
+      acc_add_word(x, b2);                          // b_2
+      Fe v = acc_reduce(x);                         // v_{2,q}
+      if (leff == 2) {
+        root = v;
+      } else if (lane == 0) {
+        // push v into level 3, carrying completed nodes upward
+        for (int j = 3; j <= leff; j++) {
+          const int li = j - 3;
+          Acc u;
+          load_acc(stk->up[li], u);
+          acc_mac_fe(u, ak[(uint64_t)(j - 1) * kM + (stk->pushed[li] & 127)], v);
+          const uint64_t pu = ++stk->pushed[li];
+          if ((pu & 127) != 0 && pu != stk->T[j - 1]) {  // node still open
+            store_acc(stk->up[li], u);
+            break;
+          }
+          acc_add_word(u, s_b[j - 1]);
+          v = acc_reduce(u);
+          acc_zero(u);
+          store_acc(stk->up[li], u);
+          if (j == leff) root = v;
+        }
+      }
+    }
+    if (t + 1 == ntiles) {
+      if (leff == 1) root = fe_shfl(root, 0);
+      if (lane == 0) store_digest<BITS>(out, si, fe_lo(root));
+    }
   }
 }
 
