@@ -667,6 +667,7 @@ struct WStack {      // lane 0's streaming state for levels 3..8
   uint64_t T[kL + 1];
   uint64_t pushed[kL - 2];
   uint32_t up[kL - 2][5];
+  uint64_t qi[32], qo0[32], qo1[32];   // metadata of the warp's current 32 work items
 };
 struct WHdr {
   uint64_t i;        // string index
@@ -695,7 +696,7 @@ PMP_DI uint4 tile_unit(uint32_t stage_s, uint32_t delta, uint32_t off) {
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(kWBlockWarps * 32)
+__global__ void __launch_bounds__(kWBlockWarps * 32, 3)
 k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
           const uint64_t *__restrict__ offsets, uint64_t n, void *__restrict__ out,
           const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
@@ -731,52 +732,90 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   lk.load(ak, r);
   const uint32_t stg_s = smem_u32(stg);
 
-  // ---- producer state (lane 0).  Work items are strided statically over the
-  // warps (item k of this warp = gw + k * nw over [big..., mid...]); lane 0
-  // keeps a two-deep metadata pipeline: the list entry of item k+2 and the
-  // offsets of item k+1 are in flight while item k's tiles are issued.
+  // ---- work items.  Big strings (>= kBigBytes, listed first) are claimed
+  // dynamically, one at a time, by lane 0 with a one-item prefetch (a big
+  // string spans >= 16 tiles, which hides the claim latency) so that the
+  // largest strings spread evenly over the warps.  Mid strings are strided
+  // statically (item k of this warp = gw + k * nw); their metadata is fetched
+  // 32 items at a time, one per lane, into registers one batch ahead and
+  // parked in a shared-memory queue that lane 0 (the producer) reads.
   const uint32_t gw = blockIdx.x * kWBlockWarps + wib, nw = gridDim.x * kWBlockWarps;
-  auto list_at = [&](uint32_t item) -> uint64_t {
-    return item < nbig ? wlist[n - 1 - item] : wlist[item - nbig];
+  uint64_t r_i = 0, r_o0 = 0, r_o1 = 0;      // lane's item of the next batch (in flight)
+  auto fetch_batch = [&](uint32_t kbase) {   // all lanes: mid items kbase + lane
+    const uint32_t item = gw + (kbase + lane) * nw;
+    if (item < nmid) {
+      r_i = wlist[item];
+      r_o0 = offsets[r_i];
+      r_o1 = offsets[r_i + 1];
+    }
   };
+  uint32_t qbase = 0;                        // item number of queue entry 0
+  auto park_batch = [&]() {                  // all lanes: registers -> queue, fetch the next batch
+    stk->qi[lane] = r_i;
+    stk->qo0[lane] = r_o0;
+    stk->qo1[lane] = r_o1;
+    __syncwarp();
+    fetch_batch(qbase + 32);
+  };
+  fetch_batch(0);
+  park_batch();
+  // big-string claim (lane 0): the next big item, prefetched
+  bool bg_have = false;
+  uint64_t bg_i = 0, bg_o0 = 0, bg_o1 = 0;
+  auto claim_big = [&]() {
+    bg_have = false;
+    if (nbig == 0) return;
+    const uint32_t item = atomicAdd(&wcount[2], 1u);
+    if (item < nbig) {
+      bg_i = wlist[n - 1 - item];
+      bg_o0 = offsets[bg_i];
+      bg_o1 = offsets[bg_i + 1];
+      bg_have = true;
+    }
+  };
+  if (lane == 0) claim_big();
+  // producer state (lane 0): the string being issued
   uint64_t p_i = 0, p_B = 0, p_nbytes = 0;
   uintptr_t p_A = 0;
-  uint32_t p_tile = 0, p_ntiles = 0, p_delta = 0;
-  bool p_have = false;
-  uint32_t nx_item = gw;                     // next item to start issuing
-  uint64_t nx_i = 0, nx_o0 = 0, nx_o1 = 0;   // its metadata (valid if nx_item < total)
-  uint64_t nn_i = 0;                         // list entry of item nx_item + nw
-  if (lane == 0) {
-    if (nx_item < total) {
-      nx_i = list_at(nx_item);
-      nx_o0 = offsets[nx_i];
-      nx_o1 = offsets[nx_i + 1];
-    }
-    if (nx_item + nw < total) nn_i = list_at(nx_item + nw);
-  }
+  uint32_t p_tile = 0, p_ntiles = 0, p_delta = 0, p_item = 0;
+  bool p_have = false, p_fold = false;
   uint32_t issued = 0, consumed = 0;
+  bool need_batch = false;
   auto produce = [&]() {  // lane 0: fill free ring slots
     while (issued - consumed < (uint32_t)kWStages) {
       if (!p_have || p_tile == p_ntiles) {
-        if (nx_item >= total) return;
-        p_i = nx_i;
-        p_B = nx_o1 - nx_o0;
-        const uintptr_t sa = (uintptr_t)(bytes + nx_o0);
+        uint64_t o0, o1;
+        if (bg_have) {
+          p_i = bg_i;
+          o0 = bg_o0;
+          o1 = bg_o1;
+          claim_big();
+        } else {
+          const uint32_t item = gw + p_item * nw;
+          if (item >= nmid) return;
+          if (p_item - qbase >= 32) {        // queue exhausted: the warp must park the next batch
+            need_batch = true;
+            return;
+          }
+          const int e = (int)(p_item - qbase);
+          p_i = stk->qi[e];
+          o0 = stk->qo0[e];
+          o1 = stk->qo1[e];
+          p_item++;
+        }
+        p_B = o1 - o0;
+        const uintptr_t sa = (uintptr_t)(bytes + o0);
         p_A = sa & ~(uintptr_t)15;
         p_delta = (uint32_t)(sa & 15);
-        p_nbytes = (((uintptr_t)(bytes + nx_o1) + 15) & ~(uintptr_t)15) - p_A;
+        p_nbytes = (((uintptr_t)(bytes + o1) + 15) & ~(uintptr_t)15) - p_A;
         const uint64_t T1 = (p_B / W + 1 + 127) / 128;           // level-1 blocks
         p_ntiles = (uint32_t)((T1 + CPI - 1) / CPI);
+        // a trailing tile holding only a marker-only block (no data bytes) is
+        // folded into the previous tile unless that block opens a level-2 node
+        p_fold = p_ntiles > 1 && (uint64_t)(p_ntiles - 1) * kWTile >= p_nbytes && ((T1 - 1) & 127) != 0;
+        if (p_fold) p_ntiles--;
         p_tile = 0;
         p_have = true;
-        // advance the metadata pipeline by one item
-        nx_item += nw;
-        if (nx_item < total) {
-          nx_i = nn_i;
-          nx_o0 = offsets[nx_i];
-          nx_o1 = offsets[nx_i + 1];
-        }
-        if (nx_item + nw < total) nn_i = list_at(nx_item + nw);
       }
       const int q = (int)(issued % kWStages);
       const uint64_t off = (uint64_t)p_tile * kWTile;
@@ -785,7 +824,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       hdr[q].B = p_B;
       hdr[q].tile = p_tile;
       hdr[q].ntiles = p_ntiles;
-      hdr[q].delta = p_delta;
+      hdr[q].delta = p_delta | ((p_fold && p_tile + 1 == p_ntiles) ? 0x100u : 0u);
       hdr[q].pad = nb;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the slot
       mbar_arrive_tx(&bar[q], nb);
@@ -794,8 +833,18 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       issued++;
     }
   };
-  if (lane == 0) produce();
-  issued = __shfl_sync(FULL, issued, 0);
+  auto refill = [&]() {   // all lanes
+    for (;;) {
+      if (lane == 0) produce();
+      issued = __shfl_sync(FULL, issued, 0);
+      const bool nb = __shfl_sync(FULL, (int)need_batch, 0) != 0;
+      if (!nb) break;
+      if (lane == 0) need_batch = false;
+      qbase += 32;
+      park_batch();
+    }
+  };
+  refill();
 
   // ---- consumer state (whole warp): the string being hashed
   uint64_t tlast = 0, T1 = 0;
@@ -808,7 +857,8 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     const int q = (int)(consumed % kWStages);
     mbar_wait(&bar[q], (consumed / kWStages) & 1);
     const uint64_t si = hdr[q].i;
-    const uint32_t t = hdr[q].tile, ntiles = hdr[q].ntiles, delta = hdr[q].delta;
+    const uint32_t t = hdr[q].tile, ntiles = hdr[q].ntiles, delta = hdr[q].delta & 15;
+    const bool fold = (hdr[q].delta & 0x100u) != 0; // + the string's marker-only last block
     const bool nodata = hdr[q].pad == 0;            // only the marker word (= 1) at word 128*c0
     if (t == 0) {                                   // a new string starts
       const uint64_t B = hdr[q].B;
@@ -872,8 +922,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     __syncwarp();
     // the slot is free: let lane 0 refill the ring before the reductions
     consumed++;
-    if (lane == 0) produce();
-    issued = __shfl_sync(FULL, issued, 0);
+    refill();
     // ---- combine the 8 lanes of each group, fold into level 2 ----
 #pragma unroll
     for (int cs = 0; cs < CPG; cs++) {
@@ -891,8 +940,16 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
         acc_mac_partial(acc2, s_a2[c & 127], x);    // a_{2, c mod 128} * v_1(c), v_1 3->2-reduced
       }
     }
+    if (fold && lane == 0) {
+      // marker-only last block c = T1 - 1: sigma = (1, 0, ..., 0), sum b_1 + a_{1,0}
+      Acc x;
+      acc_zero(x);
+      acc_add_word(x, b1);
+      acc_add_word(x, a10);
+      acc_mac_partial(acc2, s_a2[(T1 - 1) & 127], x);
+    }
     // ---- close a level-2 node every 128 blocks and at the end of the string
-    const uint64_t cend = c0 + CPI;
+    const uint64_t cend = fold ? T1 : c0 + CPI;
     if (leff >= 2 && ((cend & 127) == 0 || cend >= T1)) {
       Acc x = acc2;
 #pragma unroll
