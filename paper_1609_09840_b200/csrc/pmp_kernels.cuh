@@ -236,6 +236,26 @@ PMP_DI void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+PMP_DI void mbar_wait_s(uint32_t bar_s, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "PMP_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra PMP_WAITS_%=;\n}" ::"r"(bar_s),
+      "r"(parity)
+      : "memory");
+}
+PMP_DI void mbar_arrive_s(uint32_t bar_s) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_s) : "memory");
+}
+PMP_DI void lds_u64x2(uint32_t a, uint64_t &x, uint64_t &y) {  // two consecutive u64 (8-byte aligned)
+  asm volatile("ld.shared.u64 %0, [%2];\n\tld.shared.u64 %1, [%2+8];" : "=l"(x), "=l"(y) : "r"(a));
+}
+PMP_DI void lds_hdr(uint32_t a, uint64_t &alo, uint32_t &pos, uint32_t &mode) {  // 16-byte TileHdr
+  uint32_t x, y;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(pos), "=r"(mode) : "r"(a));
+  alo = ((uint64_t)y << 32) | x;
+}
 PMP_DI void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -257,7 +277,7 @@ PMP_DI void mbar_arrive(uint64_t *bar) {
 constexpr int kPasses = 1;                                     // strings per consumer lane per tile
 constexpr int kTile = 32 * kShortWarps * kPasses;              // 384
 constexpr int kRing = 8, kOffAhead = 4;
-constexpr uint32_t kByteRing = 40 * 1024;
+constexpr uint32_t kByteRing = 64 * 1024;
 constexpr uint32_t kSpanMaxTile = 32 * 1024;                   // larger spans go direct
 constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
 constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
@@ -369,68 +389,64 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     return;
   }
   // -------------------------------------------------------------- consumer warps
+  // shared-window addresses computed once (the loop uses explicit ld.shared)
   const uint32_t ring_s = smem_u32(ring);
+  const uint32_t offs_s = smem_u32(offs) + 8u * (32u * wib + lane);
+  const uint32_t hdr_s = smem_u32(hdr), full_s = smem_u32(bar_full), done_s = smem_u32(bar_done);
   const uint64_t tstride = (uint64_t)gridDim.x * kTile;
-  uint64_t i = (uint64_t)blockIdx.x * kTile + 32 * wib + lane;  // (tile base + lane slot)
+  uint64_t i = (uint64_t)blockIdx.x * kTile + 32 * wib + lane;
   for (uint32_t k = 0; k < my_tiles; k++, i += tstride) {
-    const int q = (int)(k & (kRing - 1));
-    mbar_wait(&bar_full[q], (k / kRing) & 1);
-    const uint32_t mode = hdr[q].mode;
-    const uint32_t rpos = hdr[q].pos;
-    const uintptr_t ralo = (uintptr_t)hdr[q].alo;
-#pragma unroll 1
-    for (int pass = 0; pass < kPasses; pass++) {
-      const uint32_t jj = 32 * (wib * kPasses + pass) + lane;  // 32 consecutive strings per pass
-      const uint64_t ii = i - (32 * wib + lane) + jj;
-      const bool valid = ii < n;
-      const uint64_t *o = offs + (size_t)q * (kOffBytes / 8) + jj;
-      uint64_t o0 = 0, Bl = 0;
-      if (valid) {
-        o0 = o[0];
-        Bl = o[1] - o0;
+    const uint32_t q = k & (kRing - 1);
+    mbar_wait_s(full_s + 8 * q, (k / kRing) & 1);
+    uint64_t ralo;
+    uint32_t rpos, mode;
+    lds_hdr(hdr_s + 16 * q, ralo, rpos, mode);
+    const bool valid = i < n;
+    uint64_t o0, o1;
+    lds_u64x2(offs_s + q * kOffBytes, o0, o1);      // offsets[i], offsets[i+1] (slot-local)
+    const uint64_t Bl = valid ? o1 - o0 : 0;
+    const bool is_short = Bl <= kShortMax;           // invalid lanes: an empty string, not stored
+    const bool is_long = !is_short;
+    const uint32_t B = (uint32_t)Bl;
+    const unsigned longmask = __ballot_sync(FULL, is_long);
+    if (longmask) {
+      // warp-aggregated append: big strings from the back, others from the front
+      const bool big = is_long && Bl >= kBigBytes;
+      const unsigned bigmask = __ballot_sync(FULL, big), midmask = longmask & ~bigmask;
+      uint32_t mbase = 0, bbase = 0;
+      if (lane == 0) {
+        if (midmask) mbase = atomicAdd(&wcount[0], (uint32_t)__popc(midmask));
+        if (bigmask) bbase = atomicAdd(&wcount[1], (uint32_t)__popc(bigmask));
       }
-      const bool is_short = valid && Bl <= kShortMax;
-      const bool is_long = valid && !is_short;
-      const uint32_t B = (uint32_t)(is_short ? Bl : 0);
-      const unsigned longmask = __ballot_sync(FULL, is_long);
-      if (longmask) {
-        // warp-aggregated append: big strings from the back, others from the front
-        const bool big = is_long && Bl >= kBigBytes;
-        const unsigned bigmask = __ballot_sync(FULL, big), midmask = longmask & ~bigmask;
-        uint32_t mbase = 0, bbase = 0;
-        if (lane == 0) {
-          if (midmask) mbase = atomicAdd(&wcount[0], (uint32_t)__popc(midmask));
-          if (bigmask) bbase = atomicAdd(&wcount[1], (uint32_t)__popc(bigmask));
-        }
-        mbase = __shfl_sync(FULL, mbase, 0);
-        bbase = __shfl_sync(FULL, bbase, 0);
-        const unsigned lt = (1u << lane) - 1;
-        if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)ii;
-        if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)ii;
+      mbase = __shfl_sync(FULL, mbase, 0);
+      bbase = __shfl_sync(FULL, bbase, 0);
+      const unsigned lt = (1u << lane) - 1;
+      if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
+      if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
+    }
+    // warp max of the number of full words (the marker word is handled apart)
+    const int tfm = (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
+    if (is_short) {
+      uint64_t lo;
+      if (mode == 0) {
+        // (lanes past n read the tile's first bytes: in bounds, result not stored)
+        const uint32_t sofs = rpos + (valid ? (uint32_t)((uintptr_t)(bytes + o0) - (uintptr_t)ralo) : 0u);
+        const uint32_t pa = ring_s + (sofs & ~3u);
+        lo = short_tree_lo<BITS>(K, skeys, B, 8 * (sofs & 3), tfm, [&](int kk) { return lds_u32(pa + 4 * kk); });
+      } else {
+        // direct tile: read the string's aligned 32-bit words straight from global,
+        // touching only words that overlap [start, end) (never past offsets[n]).
+        const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
+        const uintptr_t pa = sa & ~(uintptr_t)3;
+        lo = short_tree_lo<BITS>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, [&](int kk) {
+          const uintptr_t a = pa + 4 * (uintptr_t)kk;
+          return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
+        });
       }
-      // warp max of the number of full words (the marker word is handled apart)
-      const int tfm = (int)__reduce_max_sync(FULL, B / (BITS / 8));
-      if (is_short) {
-        uint64_t lo;
-        if (mode == 0) {
-          const uint32_t sofs = rpos + (uint32_t)((uintptr_t)(bytes + o0) - ralo);
-          const uint32_t pa = ring_s + (sofs & ~3u);
-          lo = short_tree_lo<BITS>(K, skeys, B, 8 * (sofs & 3), tfm, [&](int kk) { return lds_u32(pa + 4 * kk); });
-        } else {
-          // direct tile: read the string's aligned 32-bit words straight from global,
-          // touching only words that overlap [start, end) (never past offsets[n]).
-          const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
-          const uintptr_t pa = sa & ~(uintptr_t)3;
-          lo = short_tree_lo<BITS>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, [&](int kk) {
-            const uintptr_t a = pa + 4 * (uintptr_t)kk;
-            return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
-          });
-        }
-        store_digest<BITS>(out, ii, lo);
-      }
+      if (valid) store_digest<BITS>(out, i, lo);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&bar_done[q]);
+    if (lane == 0) mbar_arrive_s(done_s + 8 * q);
   }
 }
 
