@@ -252,11 +252,19 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if _build.needs_build() and rank == 0:
         _build.build()
+    # PMP_BENCH_BACKEND=gloo is a plumbing test for several ranks sharing one
+    # GPU (collectives on CPU tensors); real multi-GPU runs use NCCL.
+    backend = os.environ.get("PMP_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         dist.barrier()
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # device of collective tensors
     stream = torch.cuda.current_stream()
     sp = int(stream.cuda_stream)
 
@@ -279,7 +287,12 @@ def main():
             pmp._check(pmp.pmp_hash_long_partial(keys[64].handle, d_full.data_ptr(), hi - lo, lo, total,
                                                  parts[2 * rank:2 * rank + 2].data_ptr(), sp), "partial")
             if world > 1:
-                dist.all_gather_into_tensor(parts, parts[2 * rank:2 * rank + 2].clone())
+                if backend == "nccl":
+                    dist.all_gather_into_tensor(parts, parts[2 * rank:2 * rank + 2].clone())
+                else:
+                    host = parts.cpu()
+                    dist.all_gather_into_tensor(host, host[2 * rank:2 * rank + 2].clone())
+                    parts.copy_(host)
             pmp._check(pmp.pmp_hash_long_combine(keys[64].handle, parts.data_ptr(), world, total,
                                                  out.data_ptr(), sp), "combine")
         dominant = "k_node"
@@ -328,7 +341,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     k_ms, k_cnt = pmp.pmp_prof_read(dominant)
     kernel_ms = {name: pmp.pmp_prof_read(name) for name in ("k_short", "k_wstring", "k_node", "k_level", "k_combine")}
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -341,7 +354,7 @@ def main():
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, wl, pmp, keys, dev, stream, rank, world)
+        e2e = run_e2e(args, wl, pmp, keys, dev, stream, rank, world, cdev)
 
     line = None
     if rank == 0:
@@ -385,7 +398,7 @@ def fill_slice(seed, d_buf, start, sp):
     datagen.fill_device(seed, d_buf.data_ptr(), d_buf.numel(), sp, start=start)
 
 
-def run_e2e(args, wl, pmp, keys, dev, stream, rank, world):
+def run_e2e(args, wl, pmp, keys, dev, stream, rank, world, cdev):
     import torch
 
     if wl.long:
@@ -418,7 +431,7 @@ def run_e2e(args, wl, pmp, keys, dev, stream, rank, world):
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.e2e_steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=cdev)
     if world > 1:
         import torch.distributed as dist
 
