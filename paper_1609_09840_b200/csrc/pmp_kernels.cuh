@@ -676,7 +676,7 @@ PMP_HDI Geom make_geom(uint64_t Twords) {
 // Level 2 is accumulated per lane group and closed every 128 blocks; levels
 // >= 3 are streamed by lane 0 (bounded memory).
 constexpr int kWTile = 4096;
-constexpr int kWStages = 4;
+constexpr int kWStages = 3;
 constexpr int kWStageBytes = kWTile + 32;      // + 16 B overlap + 16 B read slack
 constexpr int kWBlockWarps = 4;
 struct WStack {      // lane 0's streaming state for levels 3..8
@@ -684,6 +684,13 @@ struct WStack {      // lane 0's streaming state for levels 3..8
   uint64_t pushed[kL - 2];
   uint32_t up[kL - 2][5];
   uint64_t qi[32], qo0[32], qo1[32];   // metadata of the warp's current 32 work items
+};
+struct WProd {      // lane 0's producer state (kept in shared memory, not registers)
+  uint64_t p_i, p_B, p_nbytes, p_A;
+  uint64_t bg_i, bg_o0, bg_o1;
+  uint32_t p_tile, p_ntiles, p_delta, p_item;
+  uint32_t p_have, p_fold, need_batch, bg_have;
+  uint32_t issued, pad;
 };
 struct WHdr {
   uint64_t i;        // string index
@@ -694,7 +701,7 @@ struct WHdr {
   uint32_t pad;
 };
 constexpr size_t kWSmemPerWarp =
-    ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + 127) & ~(size_t)127;
+    ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + sizeof(WProd) + 127) & ~(size_t)127;
 constexpr size_t kWSmem = 2048 /* a_2 keys, b */ + kWBlockWarps * kWSmemPerWarp;
 
 template <int BITS>
@@ -712,7 +719,7 @@ PMP_DI uint4 tile_unit(uint32_t stage_s, uint32_t delta, uint32_t off) {
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(kWBlockWarps * 32, 3)
+__global__ void __launch_bounds__(kWBlockWarps * 32, 4)
 k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
           const uint64_t *__restrict__ offsets, uint64_t n, void *__restrict__ out,
           const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
@@ -730,6 +737,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   WHdr *hdr = reinterpret_cast<WHdr *>(wbase + (size_t)kWStages * kWStageBytes);
   uint64_t *bar = reinterpret_cast<uint64_t *>(hdr + kWStages);
   WStack *stk = reinterpret_cast<WStack *>(bar + kWStages);
+  WProd *pr = reinterpret_cast<WProd *>(stk + 1);
   const uint64_t *bk = keys;           // b_1..b_8
   const uint64_t *ak = keys + kL;      // a_{j,i} at ak[(j-1)*128 + i]
   const uint32_t nmid = wcount[0], nbig = wcount[1];
@@ -776,86 +784,96 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   fetch_batch(0);
   park_batch();
   // big-string claim (lane 0): the next big item, prefetched
-  bool bg_have = false;
-  uint64_t bg_i = 0, bg_o0 = 0, bg_o1 = 0;
   auto claim_big = [&]() {
-    bg_have = false;
+    pr->bg_have = 0;
     if (nbig == 0) return;
     const uint32_t item = atomicAdd(&wcount[2], 1u);
     if (item < nbig) {
-      bg_i = wlist[n - 1 - item];
-      bg_o0 = offsets[bg_i];
-      bg_o1 = offsets[bg_i + 1];
-      bg_have = true;
+      const uint64_t bi = wlist[n - 1 - item];
+      pr->bg_i = bi;
+      pr->bg_o0 = offsets[bi];
+      pr->bg_o1 = offsets[bi + 1];
+      pr->bg_have = 1;
     }
   };
-  if (lane == 0) claim_big();
-  // producer state (lane 0): the string being issued
-  uint64_t p_i = 0, p_B = 0, p_nbytes = 0;
-  uintptr_t p_A = 0;
-  uint32_t p_tile = 0, p_ntiles = 0, p_delta = 0, p_item = 0;
-  bool p_have = false, p_fold = false;
+  if (lane == 0) {
+    pr->p_have = 0;
+    pr->p_item = 0;
+    pr->need_batch = 0;
+    pr->issued = 0;
+    claim_big();
+  }
   uint32_t issued = 0, consumed = 0;
-  bool need_batch = false;
-  auto produce = [&]() {  // lane 0: fill free ring slots
-    while (issued - consumed < (uint32_t)kWStages) {
-      if (!p_have || p_tile == p_ntiles) {
+  auto produce = [&]() {  // lane 0: fill free ring slots (state in shared memory)
+    while (pr->issued - consumed < (uint32_t)kWStages) {
+      if (!pr->p_have || pr->p_tile == pr->p_ntiles) {
         uint64_t o0, o1;
-        if (bg_have) {
-          p_i = bg_i;
-          o0 = bg_o0;
-          o1 = bg_o1;
+        if (pr->bg_have) {
+          pr->p_i = pr->bg_i;
+          o0 = pr->bg_o0;
+          o1 = pr->bg_o1;
           claim_big();
         } else {
-          const uint32_t item = gw + p_item * nw;
+          const uint32_t pi = pr->p_item;
+          const uint32_t item = gw + pi * nw;
           if (item >= nmid) return;
-          if (p_item - qbase >= 32) {        // queue exhausted: the warp must park the next batch
-            need_batch = true;
+          if (pi - qbase >= 32) {            // queue exhausted: the warp must park the next batch
+            pr->need_batch = 1;
             return;
           }
-          const int e = (int)(p_item - qbase);
-          p_i = stk->qi[e];
+          const int e = (int)(pi - qbase);
+          pr->p_i = stk->qi[e];
           o0 = stk->qo0[e];
           o1 = stk->qo1[e];
-          p_item++;
+          pr->p_item = pi + 1;
         }
-        p_B = o1 - o0;
+        const uint64_t B = o1 - o0;
         const uintptr_t sa = (uintptr_t)(bytes + o0);
-        p_A = sa & ~(uintptr_t)15;
-        p_delta = (uint32_t)(sa & 15);
-        p_nbytes = (((uintptr_t)(bytes + o1) + 15) & ~(uintptr_t)15) - p_A;
-        const uint64_t T1 = (p_B / W + 1 + 127) / 128;           // level-1 blocks
-        p_ntiles = (uint32_t)((T1 + CPI - 1) / CPI);
+        const uintptr_t A = sa & ~(uintptr_t)15;
+        const uint64_t nbytes = (((uintptr_t)(bytes + o1) + 15) & ~(uintptr_t)15) - A;
+        const uint64_t T1 = (B / W + 1 + 127) / 128;           // level-1 blocks
+        uint32_t ntiles = (uint32_t)((T1 + CPI - 1) / CPI);
         // a trailing tile holding only a marker-only block (no data bytes) is
         // folded into the previous tile unless that block opens a level-2 node
-        p_fold = p_ntiles > 1 && (uint64_t)(p_ntiles - 1) * kWTile >= p_nbytes && ((T1 - 1) & 127) != 0;
-        if (p_fold) p_ntiles--;
-        p_tile = 0;
-        p_have = true;
+        const bool fold = ntiles > 1 && (uint64_t)(ntiles - 1) * kWTile >= nbytes && ((T1 - 1) & 127) != 0;
+        if (fold) ntiles--;
+        pr->p_B = B;
+        pr->p_A = (uint64_t)A;
+        pr->p_delta = (uint32_t)(sa & 15);
+        pr->p_nbytes = nbytes;
+        pr->p_ntiles = ntiles;
+        pr->p_fold = fold;
+        pr->p_tile = 0;
+        pr->p_have = 1;
       }
-      const int q = (int)(issued % kWStages);
-      const uint64_t off = (uint64_t)p_tile * kWTile;
-      const uint32_t nb = off < p_nbytes ? (uint32_t)min((uint64_t)(kWTile + 16), p_nbytes - off) : 0u;
-      hdr[q].i = p_i;
-      hdr[q].B = p_B;
-      hdr[q].tile = p_tile;
-      hdr[q].ntiles = p_ntiles;
-      hdr[q].delta = p_delta | ((p_fold && p_tile + 1 == p_ntiles) ? 0x100u : 0u);
+      const uint32_t iss = pr->issued, tile = pr->p_tile, ntiles = pr->p_ntiles;
+      const int q = (int)(iss % kWStages);
+      const uint64_t off = (uint64_t)tile * kWTile, nbytes = pr->p_nbytes;
+      const uint32_t nb = off < nbytes ? (uint32_t)min((uint64_t)(kWTile + 16), nbytes - off) : 0u;
+      hdr[q].i = pr->p_i;
+      hdr[q].B = pr->p_B;
+      hdr[q].tile = tile;
+      hdr[q].ntiles = ntiles;
+      hdr[q].delta = pr->p_delta | ((pr->p_fold && tile + 1 == ntiles) ? 0x100u : 0u);
       hdr[q].pad = nb;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the slot
       mbar_arrive_tx(&bar[q], nb);
-      if (nb) bulk_g2s(stg + (size_t)q * kWStageBytes, reinterpret_cast<const void *>(p_A + off), nb, &bar[q]);
-      p_tile++;
-      issued++;
+      if (nb) bulk_g2s(stg + (size_t)q * kWStageBytes, reinterpret_cast<const void *>(pr->p_A + off), nb, &bar[q]);
+      pr->p_tile = tile + 1;
+      pr->issued = iss + 1;
     }
   };
   auto refill = [&]() {   // all lanes
     for (;;) {
-      if (lane == 0) produce();
+      uint32_t nb = 0;
+      if (lane == 0) {
+        produce();
+        issued = pr->issued;
+        nb = pr->need_batch;
+      }
       issued = __shfl_sync(FULL, issued, 0);
-      const bool nb = __shfl_sync(FULL, (int)need_batch, 0) != 0;
-      if (!nb) break;
-      if (lane == 0) need_batch = false;
+      if (__shfl_sync(FULL, nb, 0) == 0) break;
+      if (lane == 0) pr->need_batch = 0;
       qbase += 32;
       park_batch();
     }
