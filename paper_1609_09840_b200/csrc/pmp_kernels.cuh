@@ -701,8 +701,11 @@ struct WHdr {
   uint32_t pad;
 };
 constexpr size_t kWSmemPerWarp =
-    ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + sizeof(WProd) + 127) & ~(size_t)127;
-constexpr size_t kWSmem = 2048 /* a_2 keys, b */ + kWBlockWarps * kWSmemPerWarp;
+    ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + sizeof(WProd) + 15) & ~(size_t)15;
+// block region: a_{2,0..127}, b_1..8, and the key-only values a_{2,r} * (b_1 + a_{1,0}) mod p
+// (lo words, then hi bits) of a marker-only level-1 block at position r
+constexpr size_t kWBlockRegion = 1024 + 64 + 1024 + 512;
+constexpr size_t kWSmem = kWBlockRegion + kWBlockWarps * kWSmemPerWarp;
 
 template <int BITS>
 PMP_DI uint4 tile_unit(uint32_t stage_s, uint32_t delta, uint32_t off) {
@@ -732,7 +735,9 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   const int g = lane >> 3, r = lane & 7;
   uint64_t *s_a2 = reinterpret_cast<uint64_t *>(smem);   // a_{2,0..127}
   uint64_t *s_b = s_a2 + kM;                              // b_1..b_8
-  uint8_t *wbase = smem + 2048 + (size_t)wib * kWSmemPerWarp;
+  uint64_t *s_mklo = s_b + kL;                            // marker-only block terms (lo)
+  uint32_t *s_mkhi = reinterpret_cast<uint32_t *>(s_mklo + kM);  // (hi bit)
+  uint8_t *wbase = smem + kWBlockRegion + (size_t)wib * kWSmemPerWarp;
   uint8_t *stg = wbase;                                                   // kWStages x kWStageBytes
   WHdr *hdr = reinterpret_cast<WHdr *>(wbase + (size_t)kWStages * kWStageBytes);
   uint64_t *bar = reinterpret_cast<uint64_t *>(hdr + kWStages);
@@ -743,7 +748,21 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   const uint32_t nmid = wcount[0], nbig = wcount[1];
   const uint32_t total = nmid + nbig;
   if (total == 0) return;
-  for (int k = threadIdx.x; k < (int)kM; k += blockDim.x) s_a2[k] = ak[kM + k];
+  for (int k = threadIdx.x; k < (int)kM; k += blockDim.x) {
+    s_a2[k] = ak[kM + k];
+    // a marker-only level-1 block (sigma = 1, 0, ..., 0) has v_1 = b_1 + a_{1,0} mod p
+    Acc x, y;
+    acc_zero(x);
+    acc_add_word(x, bk[0]);
+    acc_add_word(x, ak[0]);
+    acc_zero(y);
+    acc_mac_fe(y, ak[kM + k], acc_reduce(x));
+    Fe m = acc_reduce(y);
+    uint64_t w2[2];
+    fe_store(w2, m);
+    s_mklo[k] = w2[0];
+    s_mkhi[k] = (uint32_t)w2[1];
+  }
   if (threadIdx.x < kL) s_b[threadIdx.x] = bk[threadIdx.x];
   __syncthreads();
   const uint64_t b1 = s_b[0], b2 = s_b[1], a10 = ak[0];
@@ -975,12 +994,12 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       }
     }
     if (fold && lane == 0) {
-      // marker-only last block c = T1 - 1: sigma = (1, 0, ..., 0), sum b_1 + a_{1,0}
-      Acc x;
-      acc_zero(x);
-      acc_add_word(x, b1);
-      acc_add_word(x, a10);
-      acc_mac_partial(acc2, s_a2[(T1 - 1) & 127], x);
+      // marker-only last block c = T1 - 1 (sigma = 1, 0, ..., 0): its term
+      // a_{2,c mod 128} (b_1 + a_{1,0}) mod p is key-only, precomputed per block
+      const uint64_t w2[2] = {s_mklo[(T1 - 1) & 127], s_mkhi[(T1 - 1) & 127]};
+      Fe m;
+      fe_load(w2, m);
+      acc_add_fe(acc2, m);
     }
     // ---- close a level-2 node every 128 blocks and at the end of the string
     const uint64_t cend = fold ? T1 : c0 + CPI;
