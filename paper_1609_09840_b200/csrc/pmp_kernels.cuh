@@ -23,7 +23,7 @@ namespace pmp {
 
 constexpr uint32_t kShortMax = 127;      // bytes; k_short handles B <= kShortMax
 constexpr uint32_t kBigBytes = 1u << 16; // work-list class "big" (processed first)
-constexpr int kShortWarps = 12;          // consumer warps per k_short block (+1 producer)
+constexpr int kShortWarps = 16;          // consumer warps per k_short block (+1 producer)
 constexpr int kWWarps = 4;               // warps per k_wstring / k_node block
 constexpr uint32_t FULL = 0xffffffffu;
 
