@@ -683,14 +683,19 @@ struct WStack {      // lane 0's streaming state for levels 3..8
   uint64_t T[kL + 1];
   uint64_t pushed[kL - 2];
   uint32_t up[kL - 2][5];
-  uint64_t qi[32], qo0[32], qo1[32];   // metadata of the warp's current 32 work items
+  // the warp's current 32 work items, geometry precomputed in parallel
+  uint64_t qsa[32];                    // address of the string's first byte
+  uint64_t qB[32];                     // length
+  uint32_t qi[32];                     // string index
+  uint32_t qnt[32];                    // tiles | fold flag << 31
+  uint64_t bsa, bB;                    // the claimed big string (lane 0)
+  uint32_t bi, bnt;
 };
 struct WProd {      // lane 0's producer state (kept in shared memory, not registers)
-  uint64_t p_i, p_B, p_nbytes, p_A;
-  uint64_t bg_i, bg_o0, bg_o1;
-  uint32_t p_tile, p_ntiles, p_delta, p_item;
-  uint32_t p_have, p_fold, need_batch, bg_have;
-  uint32_t issued, pad;
+  uint64_t p_sa, p_B;                  // string being issued
+  uint32_t p_i, p_nt;                  // index, tiles | fold << 31
+  uint32_t p_tile, p_item, p_have, need_batch;
+  uint32_t bg_have, issued, pq, pad;
 };
 struct WHdr {
   uint64_t i;        // string index
@@ -792,11 +797,24 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       r_o1 = offsets[r_i + 1];
     }
   };
+  // tile count of a string and whether its last tile is folded: a trailing
+  // tile holding only a marker-only block (no data bytes) is folded into the
+  // previous tile unless that block opens a level-2 node
+  auto tiles_of = [&](uint64_t sa, uint64_t B) -> uint32_t {
+    const uintptr_t A = sa & ~(uint64_t)15;
+    const uint64_t nbytes = ((sa + B + 15) & ~(uint64_t)15) - A;
+    const uint64_t T1 = (B / W + 1 + 127) / 128;           // level-1 blocks
+    uint32_t nt = (uint32_t)((T1 + CPI - 1) / CPI);
+    const bool fold = nt > 1 && (uint64_t)(nt - 1) * kWTile >= nbytes && ((T1 - 1) & 127) != 0;
+    return fold ? (nt - 1) | 0x80000000u : nt;
+  };
   uint32_t qbase = 0;                        // item number of queue entry 0
   auto park_batch = [&]() {                  // all lanes: registers -> queue, fetch the next batch
-    stk->qi[lane] = r_i;
-    stk->qo0[lane] = r_o0;
-    stk->qo1[lane] = r_o1;
+    const uint64_t sa = (uint64_t)(uintptr_t)(bytes + r_o0), B = r_o1 - r_o0;
+    stk->qsa[lane] = sa;
+    stk->qB[lane] = B;
+    stk->qi[lane] = (uint32_t)r_i;
+    stk->qnt[lane] = tiles_of(sa, B);
     __syncwarp();
     fetch_batch(qbase + 32);
   };
@@ -809,9 +827,10 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     const uint32_t item = atomicAdd(&wcount[2], 1u);
     if (item < nbig) {
       const uint64_t bi = wlist[n - 1 - item];
-      pr->bg_i = bi;
-      pr->bg_o0 = offsets[bi];
-      pr->bg_o1 = offsets[bi + 1];
+      const uint64_t o0 = offsets[bi], o1 = offsets[bi + 1];
+      stk->bsa = (uint64_t)(uintptr_t)(bytes + o0);
+      stk->bB = o1 - o0;
+      stk->bi = (uint32_t)bi;
       pr->bg_have = 1;
     }
   };
@@ -820,67 +839,61 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     pr->p_item = 0;
     pr->need_batch = 0;
     pr->issued = 0;
+    pr->pq = 0;
     claim_big();
   }
   uint32_t issued = 0, consumed = 0;
   auto produce = [&]() {  // lane 0: fill free ring slots (state in shared memory)
-    while (pr->issued - consumed < (uint32_t)kWStages) {
-      if (!pr->p_have || pr->p_tile == pr->p_ntiles) {
-        uint64_t o0, o1;
+    uint32_t iss = pr->issued, pq = pr->pq;
+    while (iss - consumed < (uint32_t)kWStages) {
+      uint32_t tile = pr->p_tile;
+      if (!pr->p_have || tile == (pr->p_nt & 0x7fffffffu)) {
         if (pr->bg_have) {
-          pr->p_i = pr->bg_i;
-          o0 = pr->bg_o0;
-          o1 = pr->bg_o1;
+          pr->p_sa = stk->bsa;
+          pr->p_B = stk->bB;
+          pr->p_i = stk->bi;
+          pr->p_nt = tiles_of(stk->bsa, stk->bB);
           claim_big();
         } else {
           const uint32_t pi = pr->p_item;
           const uint32_t item = gw + pi * nw;
-          if (item >= nmid) return;
+          if (item >= nmid) break;
           if (pi - qbase >= 32) {            // queue exhausted: the warp must park the next batch
             pr->need_batch = 1;
-            return;
+            break;
           }
           const int e = (int)(pi - qbase);
+          pr->p_sa = stk->qsa[e];
+          pr->p_B = stk->qB[e];
           pr->p_i = stk->qi[e];
-          o0 = stk->qo0[e];
-          o1 = stk->qo1[e];
+          pr->p_nt = stk->qnt[e];
           pr->p_item = pi + 1;
         }
-        const uint64_t B = o1 - o0;
-        const uintptr_t sa = (uintptr_t)(bytes + o0);
-        const uintptr_t A = sa & ~(uintptr_t)15;
-        const uint64_t nbytes = (((uintptr_t)(bytes + o1) + 15) & ~(uintptr_t)15) - A;
-        const uint64_t T1 = (B / W + 1 + 127) / 128;           // level-1 blocks
-        uint32_t ntiles = (uint32_t)((T1 + CPI - 1) / CPI);
-        // a trailing tile holding only a marker-only block (no data bytes) is
-        // folded into the previous tile unless that block opens a level-2 node
-        const bool fold = ntiles > 1 && (uint64_t)(ntiles - 1) * kWTile >= nbytes && ((T1 - 1) & 127) != 0;
-        if (fold) ntiles--;
-        pr->p_B = B;
-        pr->p_A = (uint64_t)A;
-        pr->p_delta = (uint32_t)(sa & 15);
-        pr->p_nbytes = nbytes;
-        pr->p_ntiles = ntiles;
-        pr->p_fold = fold;
-        pr->p_tile = 0;
         pr->p_have = 1;
+        tile = 0;
       }
-      const uint32_t iss = pr->issued, tile = pr->p_tile, ntiles = pr->p_ntiles;
-      const int q = (int)(iss % kWStages);
-      const uint64_t off = (uint64_t)tile * kWTile, nbytes = pr->p_nbytes;
+      const uint64_t sa = pr->p_sa, B = pr->p_B;
+      const uint32_t nt = pr->p_nt, ntiles = nt & 0x7fffffffu;
+      const uint64_t A = sa & ~(uint64_t)15;
+      const uint64_t nbytes = ((sa + B + 15) & ~(uint64_t)15) - A;
+      const int q = (int)pq;
+      pq = pq + 1 == (uint32_t)kWStages ? 0u : pq + 1;
+      const uint64_t off = (uint64_t)tile * kWTile;
       const uint32_t nb = off < nbytes ? (uint32_t)min((uint64_t)(kWTile + 16), nbytes - off) : 0u;
       hdr[q].i = pr->p_i;
-      hdr[q].B = pr->p_B;
+      hdr[q].B = B;
       hdr[q].tile = tile;
       hdr[q].ntiles = ntiles;
-      hdr[q].delta = pr->p_delta | ((pr->p_fold && tile + 1 == ntiles) ? 0x100u : 0u);
+      hdr[q].delta = (uint32_t)(sa & 15) | (((nt >> 31) && tile + 1 == ntiles) ? 0x100u : 0u);
       hdr[q].pad = nb;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the slot
       mbar_arrive_tx(&bar[q], nb);
-      if (nb) bulk_g2s(stg + (size_t)q * kWStageBytes, reinterpret_cast<const void *>(pr->p_A + off), nb, &bar[q]);
+      if (nb) bulk_g2s(stg + (size_t)q * kWStageBytes, reinterpret_cast<const void *>(A + off), nb, &bar[q]);
       pr->p_tile = tile + 1;
-      pr->issued = iss + 1;
+      iss++;
     }
+    pr->issued = iss;
+    pr->pq = pq;
   };
   auto refill = [&]() {   // all lanes
     for (;;) {
@@ -906,9 +919,14 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   Acc acc2;
   acc_zero(acc2);
   Fe root = Fe();
+  uint32_t cq = 0, cph = 0;                        // consumer slot and phase
   while (consumed < issued) {
-    const int q = (int)(consumed % kWStages);
-    mbar_wait(&bar[q], (consumed / kWStages) & 1);
+    const int q = (int)cq;
+    mbar_wait(&bar[q], cph);
+    if (++cq == (uint32_t)kWStages) {
+      cq = 0;
+      cph ^= 1;
+    }
     const uint64_t si = hdr[q].i;
     const uint32_t t = hdr[q].tile, ntiles = hdr[q].ntiles, delta = hdr[q].delta & 15;
     const bool fold = (hdr[q].delta & 0x100u) != 0; // + the string's marker-only last block
@@ -933,8 +951,22 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     const uint64_t c0 = (uint64_t)t * CPI;          // first level-1 block of this tile
     uint4 U[8];
     if (!nodata) {
+      const uint32_t ub = st_s + 1024 * g + 16 * r;  // this lane's unit j is at ub + 128 j (+ delta)
+      if (delta == 0) {                              // warp-uniform: aligned string
 #pragma unroll
-      for (int j = 0; j < 8; j++) U[j] = tile_unit<BITS>(st_s, delta, 1024 * g + 16 * (r + 8 * j));
+        for (int j = 0; j < 8; j++)
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(U[j].x), "=r"(U[j].y), "=r"(U[j].z), "=r"(U[j].w) : "r"(ub + 128 * j));
+      } else {                                       // realign: 5 aligned words + funnel shifts
+        const uint32_t a0 = ub + (delta & ~3u), sh = 8 * (delta & 3);
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const uint32_t a = a0 + 128 * j;
+          const uint32_t y0 = lds_u32(a), y1 = lds_u32(a + 4), y2 = lds_u32(a + 8), y3 = lds_u32(a + 12),
+                         y4 = lds_u32(a + 16);
+          U[j] = make_uint4(funnel(y0, y1, sh), funnel(y1, y2, sh), funnel(y2, y3, sh), funnel(y3, y4, sh));
+        }
+      }
       if (tlast < (c0 + CPI) * 128) {               // warp-uniform: the tile holds the marker word
         const uint64_t tw0 = (c0 + (uint64_t)g * CPG) * 128;
 #pragma unroll
