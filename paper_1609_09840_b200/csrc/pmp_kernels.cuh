@@ -676,7 +676,7 @@ PMP_HDI Geom make_geom(uint64_t Twords) {
 // Level 2 is accumulated per lane group and closed every 128 blocks; levels
 // >= 3 are streamed by lane 0 (bounded memory).
 constexpr int kWTile = 4096;
-constexpr int kWStages = 3;
+constexpr int kWStages = 2;
 constexpr int kWStageBytes = kWTile + 32;      // + 16 B overlap + 16 B read slack
 constexpr int kWBlockWarps = 4;
 struct WStack {      // lane 0's streaming state for levels 3..8
@@ -709,7 +709,7 @@ constexpr size_t kWSmemPerWarp =
     ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + sizeof(WProd) + 15) & ~(size_t)15;
 // block region: a_{2,0..127}, b_1..8, and the key-only values a_{2,r} * (b_1 + a_{1,0}) mod p
 // (lo words, then hi bits) of a marker-only level-1 block at position r
-constexpr size_t kWBlockRegion = 1024 + 64 + 1024 + 512;
+constexpr size_t kWBlockRegion = 1024 + 64 + 1024 + 512 + 1024 /* a_{1,0..127} */;
 constexpr size_t kWSmem = kWBlockRegion + kWBlockWarps * kWSmemPerWarp;
 
 template <int BITS>
@@ -727,7 +727,7 @@ PMP_DI uint4 tile_unit(uint32_t stage_s, uint32_t delta, uint32_t off) {
 }
 
 template <int BITS>
-__global__ void __launch_bounds__(kWBlockWarps * 32, 4)
+__global__ void __launch_bounds__(kWBlockWarps * 32, 5)
 k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
           const uint64_t *__restrict__ offsets, uint64_t n, void *__restrict__ out,
           const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
@@ -742,6 +742,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   uint64_t *s_b = s_a2 + kM;                              // b_1..b_8
   uint64_t *s_mklo = s_b + kL;                            // marker-only block terms (lo)
   uint32_t *s_mkhi = reinterpret_cast<uint32_t *>(s_mklo + kM);  // (hi bit)
+  uint64_t *s_a1 = reinterpret_cast<uint64_t *>(s_mkhi + kM);    // a_{1,0..127} (u64 or packed u32)
   uint8_t *wbase = smem + kWBlockRegion + (size_t)wib * kWSmemPerWarp;
   uint8_t *stg = wbase;                                                   // kWStages x kWStageBytes
   WHdr *hdr = reinterpret_cast<WHdr *>(wbase + (size_t)kWStages * kWStageBytes);
@@ -769,15 +770,18 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     s_mkhi[k] = (uint32_t)w2[1];
   }
   if (threadIdx.x < kL) s_b[threadIdx.x] = bk[threadIdx.x];
+  for (int k = threadIdx.x; k < (int)kM; k += blockDim.x) {
+    if constexpr (BITS == 64) s_a1[k] = ak[k];
+    else reinterpret_cast<uint32_t *>(s_a1)[k] = (uint32_t)ak[k];
+  }
   __syncthreads();
   const uint64_t b1 = s_b[0], b2 = s_b[1], a10 = ak[0];
+  const uint32_t a1_s = smem_u32(s_a1);
   if (lane == 0) {
     for (int q = 0; q < kWStages; q++) mbar_init(&bar[q], 1);
     mbar_fence_init();
   }
   __syncwarp();
-  LaneKeys<BITS> lk;
-  lk.load(ak, r);
   const uint32_t stg_s = smem_u32(stg);
 
   // ---- work items.  Big strings (>= kBigBytes, listed first) are claimed
@@ -987,19 +991,25 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       macc_zero(A);
 #pragma unroll
       for (int j = 0; j < 8; j++) {
-        mac64(A, (uint32_t)lk.k[2 * j], (uint32_t)(lk.k[2 * j] >> 32), U[j].x, U[j].y);
-        mac64(A, (uint32_t)lk.k[2 * j + 1], (uint32_t)(lk.k[2 * j + 1] >> 32), U[j].z, U[j].w);
+        uint4 kk;  // a_{1,2u}, a_{1,2u+1} for this lane's unit u = r + 8j (block-shared copy)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
+                     : "r"(a1_s + 16 * (r + 8 * j)));
+        mac64(A, kk.x, kk.y, U[j].x, U[j].y);
+        mac64(A, kk.z, kk.w, U[j].z, U[j].w);
       }
       part[0] = macc_normalize(A);
     } else {
       Acc3 A[2] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
       for (int j = 0; j < 8; j++) {
-        const int cs = j >> 2, kb = 4 * (j & 3);
-        mac32(A[cs], lk.k[kb + 0], U[j].x);
-        mac32(A[cs], lk.k[kb + 1], U[j].y);
-        mac32(A[cs], lk.k[kb + 2], U[j].z);
-        mac32(A[cs], lk.k[kb + 3], U[j].w);
+        const int cs = j >> 2;
+        uint4 kk;  // a_{1,4u'..4u'+3}, u' = r + 8 (j mod 4), packed u32 copy
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
+                     : "r"(a1_s + 16 * (r + 8 * (j & 3))));
+        mac32(A[cs], kk.x, U[j].x);
+        mac32(A[cs], kk.y, U[j].y);
+        mac32(A[cs], kk.z, U[j].z);
+        mac32(A[cs], kk.w, U[j].w);
       }
       part[0] = A[0];
       part[CPG - 1] = A[1];
