@@ -248,6 +248,9 @@ PMP_DI void mbar_wait_s(uint32_t bar_s, uint32_t parity) {
 PMP_DI void mbar_arrive_s(uint32_t bar_s) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_s) : "memory");
 }
+PMP_DI void lds_u32x2(uint32_t a, uint32_t &x, uint32_t &y) {  // 8-byte aligned
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "r"(a));
+}
 PMP_DI void lds_u64x2(uint32_t a, uint64_t &x, uint64_t &y) {  // two consecutive u64 (8-byte aligned)
   asm volatile("ld.shared.u64 %0, [%2];\n\tld.shared.u64 %1, [%2+8];" : "=l"(x), "=l"(y) : "r"(a));
 }
@@ -963,12 +966,26 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
                        : "=r"(U[j].x), "=r"(U[j].y), "=r"(U[j].z), "=r"(U[j].w) : "r"(ub + 128 * j));
       } else {                                       // realign: 5 aligned words + funnel shifts
         const uint32_t a0 = ub + (delta & ~3u), sh = 8 * (delta & 3);
+        if ((delta & 4) == 0) {                      // a0 is 8-byte aligned: (y0,y1) (y2,y3) y4
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-          const uint32_t a = a0 + 128 * j;
-          const uint32_t y0 = lds_u32(a), y1 = lds_u32(a + 4), y2 = lds_u32(a + 8), y3 = lds_u32(a + 12),
-                         y4 = lds_u32(a + 16);
-          U[j] = make_uint4(funnel(y0, y1, sh), funnel(y1, y2, sh), funnel(y2, y3, sh), funnel(y3, y4, sh));
+          for (int j = 0; j < 8; j++) {
+            const uint32_t a = a0 + 128 * j;
+            uint32_t y0, y1, y2, y3;
+            lds_u32x2(a, y0, y1);
+            lds_u32x2(a + 8, y2, y3);
+            const uint32_t y4 = lds_u32(a + 16);
+            U[j] = make_uint4(funnel(y0, y1, sh), funnel(y1, y2, sh), funnel(y2, y3, sh), funnel(y3, y4, sh));
+          }
+        } else {                                     // a0 + 4 is 8-byte aligned: y0 (y1,y2) (y3,y4)
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            const uint32_t a = a0 + 128 * j;
+            uint32_t y1, y2, y3, y4;
+            const uint32_t y0 = lds_u32(a);
+            lds_u32x2(a + 4, y1, y2);
+            lds_u32x2(a + 12, y3, y4);
+            U[j] = make_uint4(funnel(y0, y1, sh), funnel(y1, y2, sh), funnel(y2, y3, sh), funnel(y3, y4, sh));
+          }
         }
       }
       if (tlast < (c0 + CPI) * 128) {               // warp-uniform: the tile holds the marker word
@@ -1001,15 +1018,18 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     } else {
       Acc3 A[2] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int cs = j >> 2;
-        uint4 kk;  // a_{1,4u'..4u'+3}, u' = r + 8 (j mod 4), packed u32 copy
+      for (int jj = 0; jj < 4; jj++) {
+        uint4 kk;  // a_{1,4u..4u+3}, u = r + 8 jj (packed u32 copy), same for both blocks
         asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
-                     : "r"(a1_s + 16 * (r + 8 * (j & 3))));
-        mac32(A[cs], kk.x, U[j].x);
-        mac32(A[cs], kk.y, U[j].y);
-        mac32(A[cs], kk.z, U[j].z);
-        mac32(A[cs], kk.w, U[j].w);
+                     : "r"(a1_s + 16 * (r + 8 * jj)));
+#pragma unroll
+        for (int cs = 0; cs < 2; cs++) {
+          const uint4 &u = U[jj + 4 * cs];
+          mac32(A[cs], kk.x, u.x);
+          mac32(A[cs], kk.y, u.y);
+          mac32(A[cs], kk.z, u.z);
+          mac32(A[cs], kk.w, u.w);
+        }
       }
       part[0] = A[0];
       part[CPG - 1] = A[1];
