@@ -125,11 +125,8 @@ PMP_DI void acc_mac_partial(Acc3 &acc, uint64_t a, const Acc3 &x) {
 }
 // levels of Algorithm 1 applied to T words: 0 if T == 1, else ceil(log_128 T)
 PMP_HDI int levels_of(uint64_t T) {
-#ifdef __CUDA_ARCH__
-  return T <= 1 ? 0 : (64 - __clzll((long long)(T - 1)) + 6) / 7;
-#else
-  return T <= 1 ? 0 : (64 - __builtin_clzll(T - 1) + 6) / 7;
-#endif
+  return (T > 1) + (T > (1ULL << 7)) + (T > (1ULL << 14)) + (T > (1ULL << 21)) + (T > (1ULL << 28)) +
+         (T > (1ULL << 35)) + (T > (1ULL << 42)) + (T > (1ULL << 49));
 }
 
 template <int BITS> PMP_DI void store_digest(void *out, uint64_t i, uint64_t lo);
