@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--impl", default="pmp", choices=["pmp", "reference"])
     ap.add_argument("--workload", default="hashtable", choices=sorted(datagen.WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--buckets", type=int, default=0,
+                    help="hash-table consumer (SURVEY 8(f3)): write digest mod M + histogram instead of digests")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -311,10 +313,17 @@ def main():
             outs[b] = torch.empty(n, dtype=torch.int64 if b == 64 else torch.int32, device=dev)
         payload_bytes = total_bytes * len(wl.bits)
 
+        counts = torch.zeros(max(args.buckets, 1), dtype=torch.int32, device=dev)
+
         def step():
             for b in wl.bits:
-                pmp._check(pmp.pmp_hash_batch(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
-                                              outs[b].data_ptr(), sp), "pmp_hash_batch")
+                if args.buckets:
+                    pmp._check(pmp.pmp_hash_batch_buckets(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
+                                                          args.buckets, outs[b].data_ptr(), counts.data_ptr(), sp),
+                               "pmp_hash_batch_buckets")
+                else:
+                    pmp._check(pmp.pmp_hash_batch(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
+                                                  outs[b].data_ptr(), sp), "pmp_hash_batch")
         dominant = "k_short" if wl.hi <= 127 else "k_wstring"
         # algorithmic bytes per dominant launch: payload + offsets + digests (avg over widths)
         alg_bytes_per_launch = total_bytes + 8 * (n + 1) + n * sum(b // 8 for b in wl.bits) / len(wl.bits)
@@ -373,7 +382,8 @@ def main():
             "scaling": "strong" if wl.long else "weak", "vs_baseline": None,
             "dtype": "u64+u32" if len(wl.bits) > 1 else f"u{wl.bits[0]}",
             "data": "synthetic (seeded xoshiro256** bytes, generated on device)",
-            "config": workload_config(wl, world),
+            "config": dict(workload_config(wl, world), **({"output": f"buckets mod {args.buckets} + histogram"}
+                                                          if args.buckets else {})),
             "bytes_per_gpu_cycle": (value / world * 1e9) / (clocks["sm_mhz"] * 1e6) if clocks.get("sm_mhz") else None,
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s",

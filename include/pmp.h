@@ -87,6 +87,18 @@ void pmp_keys_free(pmp_keys *keys);
 int pmp_hash_batch(const pmp_keys *keys, const uint8_t *bytes, const uint64_t *offsets,
                    uint64_t n, void *out, struct CUstream_st *stream);
 
+/* Hash-table consumer: the same batch hash, fused with the
+ * bucket mapping b_i = digest_i mod M (M >= 1).  By the paper's lemmas the
+ * bucket map keeps almost Delta-universality up to a factor ceil((2|Y|-1)/M)
+ * and is 2-regular, regular when M divides 2^n.
+ *   buckets (device) n uint32;
+ *   counts  (device) M uint32 incremented atomically per string (the caller
+ *           zeroes it; histograms of several calls accumulate), or NULL.
+ * Same conventions and errors as pmp_hash_batch; PMP_EINVAL for M == 0. */
+int pmp_hash_batch_buckets(const pmp_keys *keys, const uint8_t *bytes, const uint64_t *offsets,
+                           uint64_t n, uint32_t M, uint32_t *buckets, uint32_t *counts,
+                           struct CUstream_st *stream);
+
 /* Hash one string of `len` bytes at `bytes` (device, any alignment); writes
  * one digest (uint64 / uint32) to `out` (device).  Block-parallel over the
  * level-2 nodes of the tree (128 level-1 blocks each), then one launch per

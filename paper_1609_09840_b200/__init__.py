@@ -44,6 +44,7 @@ def lib() -> ctypes.CDLL:
             "pmp_keys_bits": ([_vp], _int),
             "pmp_keys_free": ([_vp], None),
             "pmp_hash_batch": ([_vp, _vp, _vp, _u64, _vp, _vp], _int),
+            "pmp_hash_batch_buckets": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _vp, _vp], _int),
             "pmp_hash_long": ([_vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_long_partial": ([_vp, _vp, _u64, _u64, _u64, _vp, _vp], _int),
             "pmp_hash_long_combine": ([_vp, _vp, _int, _u64, _vp, _vp], _int),
@@ -92,6 +93,11 @@ def pmp_keys_free(keys: int) -> None:
 
 def pmp_hash_batch(keys: int, bytes_ptr: int, offsets_ptr: int, n: int, out_ptr: int, stream: int) -> int:
     return lib().pmp_hash_batch(keys, bytes_ptr, offsets_ptr, n, out_ptr, stream)
+
+
+def pmp_hash_batch_buckets(keys: int, bytes_ptr: int, offsets_ptr: int, n: int, M: int, buckets_ptr: int,
+                           counts_ptr: int, stream: int) -> int:
+    return lib().pmp_hash_batch_buckets(keys, bytes_ptr, offsets_ptr, n, M, buckets_ptr, counts_ptr, stream)
 
 
 def pmp_hash_long(keys: int, bytes_ptr: int, length: int, out_ptr: int, stream: int) -> int:
@@ -200,6 +206,20 @@ def hash_batch(keys: Keys, payload, offsets, out=None, stream=None):
                           device=offsets.device)
     _check(pmp_hash_batch(keys.handle, payload.data_ptr(), offsets.data_ptr(), max(n, 0),
                           out.data_ptr(), _stream_ptr(stream)), "pmp_hash_batch")
+    return out
+
+
+def hash_batch_buckets(keys: Keys, payload, offsets, M: int, counts=None, out=None, stream=None):
+    """Bucket ids digest mod M (int32 tensor holding uint32) and, if ``counts``
+    (int32 CUDA tensor of M zeros) is given, the per-bucket histogram."""
+    import torch
+
+    n = offsets.numel() - 1
+    if out is None:
+        out = torch.empty(max(n, 0), dtype=torch.int32, device=offsets.device)
+    _check(pmp_hash_batch_buckets(keys.handle, payload.data_ptr(), offsets.data_ptr(), max(n, 0), M,
+                                  out.data_ptr(), counts.data_ptr() if counts is not None else 0,
+                                  _stream_ptr(stream)), "pmp_hash_batch_buckets")
     return out
 
 

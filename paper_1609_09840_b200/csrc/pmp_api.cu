@@ -346,11 +346,11 @@ void pmp_keys_free(pmp_keys *k) {
   delete k;
 }
 
-int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
-                   void *out, cudaStream_t st) {
+static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
+                           const OutSpec &os, cudaStream_t st) {
   if (!k) return PMP_EINVAL;
   if (n == 0) return 0;
-  if (!bytes || !offsets || !out || n >= (1ULL << 32)) return PMP_EINVAL;
+  if (!bytes || !offsets || !os.out || n >= (1ULL << 32)) return PMP_EINVAL;
   if (int rc = check_keys(k)) return rc;
   const int sms = sm_count(k->device);
   Scratch sc(st), sc_off(st);
@@ -381,9 +381,9 @@ int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offs
   const int threads = (kShortWarps + 1) * 32;  // + producer warp
   int rc;
   if (k->bits == 64)
-    rc = launch("k_short", st, [&] { k_short<64><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
+    rc = launch("k_short", st, [&] { k_short<64><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
   else
-    rc = launch("k_short", st, [&] { k_short<32><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, out, wlist, wcount); });
+    rc = launch("k_short", st, [&] { k_short<32><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
   if (rc) return rc;
   static std::once_flag wattr_once;
   std::call_once(wattr_once, [] {
@@ -393,10 +393,29 @@ int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offs
   const uint64_t wper_sm = (228u * 1024u) / (kWSmem + 1024u);
   const unsigned wgrid = (unsigned)(sms * (wper_sm ? wper_sm : 1));  // persistent, work list drained by atomics
   if (k->bits == 64)
-    rc = launch("k_wstring", st, [&] { k_wstring<64><<<wgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, out, wlist, wcount); });
+    rc = launch("k_wstring", st, [&] { k_wstring<64><<<wgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
   else
-    rc = launch("k_wstring", st, [&] { k_wstring<32><<<wgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, out, wlist, wcount); });
+    rc = launch("k_wstring", st, [&] { k_wstring<32><<<wgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
   return rc;
+}
+
+int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
+                   void *out, cudaStream_t st) {
+  OutSpec os;
+  os.out = out;
+  os.M = 0;
+  os.counts = nullptr;
+  return hash_batch_impl(k, bytes, offsets, n, os, st);
+}
+
+int pmp_hash_batch_buckets(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
+                           uint32_t M, uint32_t *buckets, uint32_t *counts, cudaStream_t st) {
+  if (M == 0) return PMP_EINVAL;
+  OutSpec os;
+  os.out = buckets;
+  os.M = M;
+  os.counts = counts;
+  return hash_batch_impl(k, bytes, offsets, n, os, st);
 }
 
 int pmp_hash_long_partial(const pmp_keys *k, const uint8_t *local, uint64_t local_len, uint64_t g0,

@@ -129,12 +129,32 @@ PMP_HDI int levels_of(uint64_t T) {
          (T > (1ULL << 35)) + (T > (1ULL << 42)) + (T > (1ULL << 49));
 }
 
+// Where a batch digest goes: the digest itself (M == 0), or -- the hash-table
+// consumer of SURVEY 8(f3) -- its bucket digest mod M (h mod M
+// stays almost Delta-universal; it is 2-regular, regular when M | 2^n),
+// optionally counted into a device histogram.
+struct OutSpec {
+  void *out;        // n digests (uint64/uint32) or n uint32 buckets
+  uint32_t M;       // 0: digests
+  uint32_t *counts; // M counters (atomically incremented) or nullptr
+};
+
 template <int BITS> PMP_DI void store_digest(void *out, uint64_t i, uint64_t lo);
 template <> PMP_DI void store_digest<64>(void *out, uint64_t i, uint64_t lo) {
   reinterpret_cast<uint64_t *>(out)[i] = mix64(lo);
 }
 template <> PMP_DI void store_digest<32>(void *out, uint64_t i, uint64_t lo) {
   reinterpret_cast<uint32_t *>(out)[i] = mix32((uint32_t)lo);
+}
+template <int BITS> PMP_DI void emit(const OutSpec &os, uint64_t i, uint64_t lo) {
+  if (os.M == 0) {
+    store_digest<BITS>(os.out, i, lo);
+    return;
+  }
+  const uint64_t d = BITS == 64 ? mix64(lo) : (uint64_t)mix32((uint32_t)lo);
+  const uint32_t b = (uint32_t)(d % os.M);
+  reinterpret_cast<uint32_t *>(os.out)[i] = b;
+  if (os.counts) atomicAdd(&os.counts[b], 1u);
 }
 
 // ============================================================= k_short
@@ -293,7 +313,7 @@ constexpr size_t kShortSmem = 256 /* keys */ + kByteRing + kSlack + 16 + (size_t
 template <int BITS>
 __global__ void __launch_bounds__((kShortWarps + 1) * 32)
 k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets,
-        uint64_t n, void *__restrict__ out, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
+        uint64_t n, const OutSpec os, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint64_t *skeys = reinterpret_cast<uint64_t *>(smem);                       // a_{1,0..31}
@@ -443,7 +463,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
           return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
         });
       }
-      if (valid) store_digest<BITS>(out, i, lo);
+      if (valid) emit<BITS>(os, i, lo);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive_s(done_s + 8 * q);
@@ -729,7 +749,7 @@ PMP_DI uint4 tile_unit(uint32_t stage_s, uint32_t delta, uint32_t off) {
 template <int BITS>
 __global__ void __launch_bounds__(kWBlockWarps * 32, 5)
 k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
-          const uint64_t *__restrict__ offsets, uint64_t n, void *__restrict__ out,
+          const uint64_t *__restrict__ offsets, uint64_t n, const OutSpec os,
           const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
   using T = Tr<BITS>;
   using Acc = typename T::Acc;
@@ -1096,7 +1116,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     }
     if (t + 1 == ntiles) {
       if (leff == 1) root = fe_shfl(root, 0);
-      if (lane == 0) store_digest<BITS>(out, si, fe_lo(root));
+      if (lane == 0) emit<BITS>(os, si, fe_lo(root));
     }
   }
 }

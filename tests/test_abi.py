@@ -123,3 +123,8 @@ def test_long_constant_matches_oracle_tree_of_zero_blocks(L, oracle_lib, bits, l
         z = np.zeros(T1, dtype=np.uint64)
         want, _ = oracle_lib.tree_generic_np(p, 128, 8, ok.b, ok.a, z, z, j0=1)
     assert got == want
+
+
+def test_bucket_call_rejects_zero_modulus(L):
+    k = pmp.Keys.generate(1, 64)
+    assert pmp.pmp_hash_batch_buckets(k.handle, 8, 8, 1, 0, 8, 0, 0) == pmp.PMP_EINVAL

@@ -257,3 +257,30 @@ def test_long_partition_invariance(torch_dev, oracle_lib, bits):
             pmp.hash_long_partial(keys, d[b[g]:], b[g + 1] - b[g], b[g], total, partial=parts[2 * g:2 * g + 2])
         got = int(pmp.as_u64(pmp.hash_long_combine(keys, parts, total))[0])
         assert got == ref, b
+
+
+# ------------------------------------------------------------ hash-table consumer
+@pytest.mark.parametrize("bits", [32, 64])
+@pytest.mark.parametrize("M", [1, 7, 1024, 2**32 - 1])
+def test_buckets_and_histogram(torch_dev, oracle_lib, bits, M):
+    """pmp_hash_batch_buckets == oracle digest mod M, and its fused histogram ==
+    bincount, for a batch mixing short, long, empty and misaligned strings."""
+    import torch
+
+    rng = np.random.default_rng(M % 1000 + bits)
+    lens = rng.integers(0, 300, size=5000).astype(np.uint64)
+    lens[::97] = rng.integers(1000, 70000, size=lens[::97].size).astype(np.uint64)
+    off = datagen.offsets_from_lengths(lens) + 3
+    pay = datagen.payload_host(31, 0, int(off[-1]))
+    keys = pmp.Keys.generate(31, bits)
+    d_pay = torch.from_numpy(pay).to(torch_dev)
+    d_off = torch.from_numpy(off.view(np.int64)).to(torch_dev)
+    Mc = min(M, 1 << 16)
+    counts = torch.zeros(Mc, dtype=torch.int32, device=torch_dev) if M == Mc else None
+    b = pmp.hash_batch_buckets(keys, d_pay, d_off, M, counts=counts)
+    torch.cuda.synchronize()
+    got = b.cpu().numpy().view(np.uint32).astype(np.uint64)
+    want = oracle_batch(oracle_lib, 31, bits, pay, off).astype(np.uint64) % np.uint64(M)
+    assert np.array_equal(got, want)
+    if counts is not None:
+        assert np.array_equal(counts.cpu().numpy().astype(np.int64), np.bincount(want.astype(np.int64), minlength=M))
