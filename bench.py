@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--impl", default="pmp", choices=["pmp", "reference"])
     ap.add_argument("--workload", default="hashtable", choices=sorted(datagen.WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--stream-mib", type=int, default=0,
+                    help="long16g only (SURVEY 8(f1)): feed the string through pmp_stream_update in pieces of this many MiB")
     ap.add_argument("--buckets", type=int, default=0,
                     help="hash-table consumer (SURVEY 8(f3)): write digest mod M + histogram instead of digests")
     ap.add_argument("--no-cpu", action="store_true")
@@ -285,7 +287,20 @@ def main():
         out = torch.zeros(1, dtype=torch.int64, device=dev)
         payload_bytes = total
 
+        sth = pmp.pmp_stream_new(keys[64].handle) if args.stream_mib else 0
+        piece = args.stream_mib << 20
+
+        def step_stream():
+            pmp._check(pmp.pmp_stream_reset(sth, sp), "reset")
+            for pos in range(0, hi - lo, piece):
+                pmp._check(pmp.pmp_stream_update(sth, d_full.data_ptr() + pos, min(piece, hi - lo - pos), sp),
+                           "update")
+            pmp._check(pmp.pmp_stream_final(sth, out.data_ptr(), sp), "final")
+
         def step():
+            if args.stream_mib:
+                assert world == 1, "--stream-mib measures one GPU"
+                return step_stream()
             pmp._check(pmp.pmp_hash_long_partial(keys[64].handle, d_full.data_ptr(), hi - lo, lo, total,
                                                  parts[2 * rank:2 * rank + 2].data_ptr(), sp), "partial")
             if world > 1:
@@ -297,8 +312,8 @@ def main():
                     parts.copy_(host)
             pmp._check(pmp.pmp_hash_long_combine(keys[64].handle, parts.data_ptr(), world, total,
                                                  out.data_ptr(), sp), "combine")
-        dominant = "k_node"
-        alg_bytes_per_launch = hi - lo
+        dominant = "k_stream_node" if args.stream_mib else "k_node"
+        alg_bytes_per_launch = min(piece, hi - lo) if args.stream_mib else hi - lo
         n = 1
     else:
         seed, lens, offs, b0 = make_batch(wl, rank)
@@ -349,7 +364,8 @@ def main():
     launches = pmp.pmp_launch_count() - l0
     ms = ev0.elapsed_time(ev1)
     k_ms, k_cnt = pmp.pmp_prof_read(dominant)
-    kernel_ms = {name: pmp.pmp_prof_read(name) for name in ("k_short", "k_wstring", "k_node", "k_level", "k_combine")}
+    kernel_ms = {name: pmp.pmp_prof_read(name) for name in ("k_short", "k_wstring", "k_node", "k_level", "k_combine",
+                                                             "k_stream")}
     t = torch.tensor([ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -383,7 +399,8 @@ def main():
             "dtype": "u64+u32" if len(wl.bits) > 1 else f"u{wl.bits[0]}",
             "data": "synthetic (seeded xoshiro256** bytes, generated on device)",
             "config": dict(workload_config(wl, world), **({"output": f"buckets mod {args.buckets} + histogram"}
-                                                          if args.buckets else {})),
+                                                          if args.buckets else {}),
+                           **({"api": f"pmp_stream_update in {args.stream_mib} MiB pieces"} if args.stream_mib else {})),
             "bytes_per_gpu_cycle": (value / world * 1e9) / (clocks["sm_mhz"] * 1e6) if clocks.get("sm_mhz") else None,
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s",

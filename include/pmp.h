@@ -126,6 +126,26 @@ int pmp_hash_long_partial(const pmp_keys *keys, const uint8_t *local, uint64_t l
 int pmp_hash_long_combine(const pmp_keys *keys, const uint64_t *partials, int G,
                           uint64_t total_len, void *out, struct CUstream_st *stream);
 
+/* Incremental hashing (the bounded-memory evaluation of
+ * Algorithm 1).  The digest of all bytes fed through
+ * pmp_stream_update equals pmp_hash_long of their concatenation, for every way
+ * of cutting it into updates (split invariance).  Device state: one
+ * open-node running sum per level (O(L)) plus < one level-1 block of pending
+ * bytes; each update hashes its whole blocks with the block-parallel node
+ * kernel.  A stream is single-owner; calls are ordered on `stream`.
+ *   pmp_stream_new:    state on the keys' device (NULL on failure);
+ *   pmp_stream_update: `bytes` (device, any alignment, any length); the
+ *                      caller may reuse the buffer once the stream reaches it;
+ *   pmp_stream_final:  writes the digest (uint64/uint32) to `out` (device);
+ *                      further updates return PMP_EINVAL until a reset;
+ *   pmp_stream_reset:  start a new message with the same keys. */
+typedef struct pmp_stream pmp_stream;
+pmp_stream *pmp_stream_new(const pmp_keys *keys);
+int pmp_stream_update(pmp_stream *s, const uint8_t *bytes, uint64_t len, struct CUstream_st *stream);
+int pmp_stream_final(pmp_stream *s, void *out, struct CUstream_st *stream);
+int pmp_stream_reset(pmp_stream *s, struct CUstream_st *stream);
+void pmp_stream_free(pmp_stream *s);
+
 /* Host-only helper: split [0, total_len) into G contiguous ranges aligned to
  * level-1 blocks with equal block counts (+- 1); begins[0..G] (host),
  * begins[G] = total_len.  Returns 0 or PMP_EINVAL. */

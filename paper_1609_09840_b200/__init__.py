@@ -49,6 +49,11 @@ def lib() -> ctypes.CDLL:
             "pmp_hash_long_partial": ([_vp, _vp, _u64, _u64, _u64, _vp, _vp], _int),
             "pmp_hash_long_combine": ([_vp, _vp, _int, _u64, _vp, _vp], _int),
             "pmp_long_split": ([_int, _u64, _int, _vp], _int),
+            "pmp_stream_new": ([_vp], _vp),
+            "pmp_stream_update": ([_vp, _vp, _u64, _vp], _int),
+            "pmp_stream_final": ([_vp, _vp, _vp], _int),
+            "pmp_stream_reset": ([_vp, _vp], _int),
+            "pmp_stream_free": ([_vp], None),
             "pmp_long_constant": ([_vp, _u64, _vp], _int),
             "pmp_selftest": ([_int, _int, _vp, _u64, _vp, _vp], _int),
             "pmp_launch_count": ([], _u64),
@@ -113,6 +118,26 @@ def pmp_hash_long_partial(keys: int, local_ptr: int, local_len: int, global_offs
 def pmp_hash_long_combine(keys: int, partials_ptr: int, G: int, total_len: int, out_ptr: int,
                           stream: int) -> int:
     return lib().pmp_hash_long_combine(keys, partials_ptr, G, total_len, out_ptr, stream)
+
+
+def pmp_stream_new(keys: int) -> int:
+    return lib().pmp_stream_new(keys) or 0
+
+
+def pmp_stream_update(s: int, bytes_ptr: int, length: int, stream: int) -> int:
+    return lib().pmp_stream_update(s, bytes_ptr, length, stream)
+
+
+def pmp_stream_final(s: int, out_ptr: int, stream: int) -> int:
+    return lib().pmp_stream_final(s, out_ptr, stream)
+
+
+def pmp_stream_reset(s: int, stream: int) -> int:
+    return lib().pmp_stream_reset(s, stream)
+
+
+def pmp_stream_free(s: int) -> None:
+    lib().pmp_stream_free(s)
 
 
 def pmp_selftest(out_bits: int, mode: int, in_ptr: int, n: int, out_ptr: int, stream: int) -> int:
@@ -254,6 +279,45 @@ def hash_long_combine(keys: Keys, partials, total_len: int, out=None, stream=Non
     _check(pmp_hash_long_combine(keys.handle, partials.data_ptr(), G, total_len, out.data_ptr(),
                                  _stream_ptr(stream)), "pmp_hash_long_combine")
     return out
+
+
+class Stream:
+    """Incremental hash (pmp_stream_*): ``update`` with uint8 CUDA tensors, then
+    ``final`` -> digest tensor.  Keep fed tensors alive until the torch stream
+    has consumed them."""
+
+    def __init__(self, keys: Keys):
+        self.keys = keys
+        self.handle = pmp_stream_new(keys.handle)
+        if not self.handle:
+            raise PmpError(PMP_ENOMEM, "pmp_stream_new")
+
+    def update(self, data, length: int | None = None, stream=None):
+        length = data.numel() if length is None else length
+        _check(pmp_stream_update(self.handle, data.data_ptr(), length, _stream_ptr(stream)), "pmp_stream_update")
+        return self
+
+    def final(self, out=None, stream=None):
+        import torch
+
+        if out is None:
+            out = torch.empty(1, dtype=torch.int64 if self.keys.bits == 64 else torch.int32, device="cuda")
+        _check(pmp_stream_final(self.handle, out.data_ptr(), _stream_ptr(stream)), "pmp_stream_final")
+        return out
+
+    def reset(self, stream=None):
+        _check(pmp_stream_reset(self.handle, _stream_ptr(stream)), "pmp_stream_reset")
+
+    def close(self):
+        if self.handle:
+            pmp_stream_free(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def as_u64(t) -> "object":

@@ -276,8 +276,166 @@ int long_partial_impl(const pmp_keys *k, const uint8_t *local, uint64_t local_le
 
 }  // namespace
 
+struct pmp_stream {
+  const pmp_keys *k;
+  StreamState *d_state;
+  uint8_t *d_tail;      // < one level-1 block of pending bytes (+16 B read slack)
+  uint64_t *d_s2;       // scratch for node partial sums
+  size_t s2_cap;        // entries (pairs)
+  uint64_t tail_len, c_done;
+  bool finalized;
+};
+
+namespace {
+template <int BITS>
+int stream_range(pmp_stream *s, const uint8_t *base, uint64_t c0, uint64_t N, cudaStream_t st) {
+  const uint64_t CB = (uint64_t)chunk_bytes(BITS);
+  const uint64_t qb = c0 / 128, qe = (c0 + N + 127) / 128, nq = qe - qb;
+  const int sms = sm_count(s->k->device);
+  int P = 1;  // pieces per node: keep >= 32 warps per SM busy on short updates
+  while (P < 32 && nq * (uint64_t)P < (uint64_t)sms * 32) P *= 2;
+  const uint64_t need = nq * (uint64_t)P;
+  if (need > s->s2_cap) {  // s2 (nq * P partials), two merge value arrays, per-node piece counters
+    uint64_t *p = nullptr;
+    if (cudaMallocAsync(&p, 3 * need * 16 + need * 4, st) != cudaSuccess) return PMP_ENOMEM;
+    if (cudaMemsetAsync(p + 6 * need, 0, need * 4, st) != cudaSuccess) return PMP_ECUDA;
+    if (s->d_s2) cudaFreeAsync(s->d_s2, st);
+    s->d_s2 = p;
+    s->s2_cap = need;
+  }
+  StrView v;
+  v.base = base;
+  v.g0 = c0 * CB;
+  v.avail_end = v.g0 + N * CB;
+  v.B = ~0ULL;  // no marker inside an update: every block is full
+  v.delta = (uint32_t)((uintptr_t)base & 15);
+  uint64_t grid = (need + kWWarps - 1) / kWWarps;
+  if (grid > (uint64_t)sms * 16) grid = (uint64_t)sms * 16;
+  return launch("k_stream_node", st, [&] {
+    k_stream_node<BITS><<<(unsigned)grid, kWWarps * 32, 0, st>>>(s->k->d_blob, v, c0, N, qb, qe, P, s->d_s2,
+                                                                   (uint32_t *)(s->d_s2 + 6 * s->s2_cap),
+                                                                   s->d_state, s->d_s2 + 2 * s->s2_cap,
+                                                                   s->d_s2 + 4 * s->s2_cap);
+  });
+}
+
+template <int BITS>
+int stream_update(pmp_stream *s, const uint8_t *data, uint64_t len, cudaStream_t st) {
+  const uint64_t CB = (uint64_t)chunk_bytes(BITS);
+  if (s->tail_len > 0 || len < CB) {
+    const uint64_t fill = min(len, CB - s->tail_len);
+    if (fill && cudaMemcpyAsync(s->d_tail + s->tail_len, data, fill, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return PMP_ECUDA;
+    s->tail_len += fill;
+    data += fill;
+    len -= fill;
+    if (s->tail_len < CB) return 0;
+    if (int rc = stream_range<BITS>(s, s->d_tail, s->c_done, 1, st)) return rc;
+    s->c_done += 1;
+    s->tail_len = 0;
+  }
+  const uint64_t N = len / CB;
+  if (N) {
+    if (int rc = stream_range<BITS>(s, data, s->c_done, N, st)) return rc;
+    s->c_done += N;
+    data += N * CB;
+    len -= N * CB;
+  }
+  if (len) {
+    if (cudaMemcpyAsync(s->d_tail, data, len, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return PMP_ECUDA;
+    s->tail_len = len;
+  }
+  return 0;
+}
+
+template <int BITS>
+int stream_final(pmp_stream *s, void *out, cudaStream_t st) {
+  const uint64_t CB = (uint64_t)chunk_bytes(BITS);
+  const uint64_t Btot = s->c_done * CB + s->tail_len;
+  const int leff = levels_of(words_of(BITS, Btot));
+  if (s->s2_cap < 1) {
+    if (cudaMallocAsync(&s->d_s2, 3 * 16 + 4, st) != cudaSuccess) return PMP_ENOMEM;
+    if (cudaMemsetAsync(s->d_s2 + 6, 0, 4, st) != cudaSuccess) return PMP_ECUDA;
+    s->s2_cap = 1;
+  }
+  StrView v;
+  v.base = s->d_tail;
+  v.g0 = s->c_done * CB;
+  v.avail_end = v.g0 + s->tail_len;
+  v.B = Btot;
+  v.delta = 0;
+  int rc;
+  if (s->c_done == 0) {  // the whole string is in the tail: one block or less
+    v.g0 = 0;
+    rc = launch("k_node", st, [&] { k_node<BITS><<<1, kWWarps * 32, 0, st>>>(s->k->d_blob, v, 0, 1, 0, 1, 1, s->d_s2); });
+  } else {               // the last block (tail bytes + marker) of node c_done / 128
+    const uint64_t c = s->c_done;
+    rc = launch("k_node", st, [&] {
+      k_node<BITS><<<1, kWWarps * 32, 0, st>>>(s->k->d_blob, v, c, c + 1, c / 128, c / 128 + 1, 0, s->d_s2);
+    });
+  }
+  if (rc) return rc;
+  return launch("k_stream_final", st, [&] {
+    k_stream_final<BITS><<<1, 32, 0, st>>>(s->k->d_blob, s->d_state, s->d_s2, leff, out);
+  });
+}
+}  // namespace
+
 // =================================================================== C ABI
 extern "C" {
+
+pmp_stream *pmp_stream_new(const pmp_keys *k) {
+  if (!k || !k->d_blob) return nullptr;
+  pmp_stream *s = new (std::nothrow) pmp_stream;
+  if (!s) return nullptr;
+  s->k = k;
+  s->d_state = nullptr;
+  s->d_tail = nullptr;
+  s->d_s2 = nullptr;
+  s->s2_cap = 0;
+  s->tail_len = s->c_done = 0;
+  s->finalized = false;
+  if (cudaMalloc(&s->d_state, sizeof(StreamState)) != cudaSuccess ||
+      cudaMalloc(&s->d_tail, (size_t)chunk_bytes(k->bits) + 32) != cudaSuccess ||
+      cudaMemset(s->d_state, 0, sizeof(StreamState)) != cudaSuccess) {
+    if (s->d_state) cudaFree(s->d_state);
+    if (s->d_tail) cudaFree(s->d_tail);
+    delete s;
+    return nullptr;
+  }
+  return s;
+}
+
+int pmp_stream_update(pmp_stream *s, const uint8_t *bytes, uint64_t len, cudaStream_t st) {
+  if (!s || (!bytes && len) || s->finalized) return PMP_EINVAL;
+  if (len == 0) return 0;
+  const uint64_t CB = (uint64_t)chunk_bytes(s->k->bits);
+  if (words_of(s->k->bits, s->c_done * CB + s->tail_len + len) > (1ULL << 56)) return PMP_ETOOLONG;
+  return s->k->bits == 64 ? stream_update<64>(s, bytes, len, st) : stream_update<32>(s, bytes, len, st);
+}
+
+int pmp_stream_final(pmp_stream *s, void *out, cudaStream_t st) {
+  if (!s || !out || s->finalized) return PMP_EINVAL;
+  s->finalized = true;
+  return s->k->bits == 64 ? stream_final<64>(s, out, st) : stream_final<32>(s, out, st);
+}
+
+int pmp_stream_reset(pmp_stream *s, cudaStream_t st) {
+  if (!s) return PMP_EINVAL;
+  s->tail_len = s->c_done = 0;
+  s->finalized = false;
+  return cudaMemsetAsync(s->d_state, 0, sizeof(StreamState), st) == cudaSuccess ? 0 : PMP_ECUDA;
+}
+
+void pmp_stream_free(pmp_stream *s) {
+  if (!s) return;
+  cudaDeviceSynchronize();
+  cudaFree(s->d_state);
+  cudaFree(s->d_tail);
+  if (s->d_s2) cudaFree(s->d_s2);
+  delete s;
+}
+
 
 const char *pmp_strerror(int code) {
   if (code > 0 || code < -5) return "unknown error";

@@ -119,6 +119,16 @@ def test_long16g_full(dev, oracle_lib):
         for g, (b, e) in enumerate(parallel.long_ranges(64, total, G)):
             pmp.hash_long_partial(keys, buf[b:], e - b, b, total, partial=parts[2 * g:2 * g + 2])
         assert int(pmp.as_u64(pmp.hash_long_combine(keys, parts, total))[0]) == got, G
+    # streaming (8(f1)): one 16 GiB update (1 piece per node) and ~1 GiB misaligned
+    # pieces (8 pieces per node, level-3/4 nodes closing across updates)
+    for cuts in ([total], [(1 << 30) + 4099] * 15 + [total - 15 * ((1 << 30) + 4099)]):
+        st = pmp.Stream(keys)
+        pos = 0
+        for c in cuts:
+            st.update(buf[pos:], c)
+            pos += c
+        assert int(pmp.as_u64(st.final())[0]) == got, len(cuts)
+        st.close()
     del buf
     torch.cuda.empty_cache()
     host = host_payload_parallel(wl.seed, 0, total)

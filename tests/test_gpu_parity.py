@@ -309,3 +309,75 @@ def test_single_word_sweep_regularity(torch_dev, oracle_lib, bits):
     keys = pmp.Keys.generate(78, bits)
     coll = quality.word_sweep(keys, 1 << 24, seed=6)
     assert 0 <= coll <= quality.bound(bits)
+
+
+# ------------------------------------------------------------ streaming
+@pytest.mark.parametrize("bits", [32, 64])
+def test_stream_split_invariance(torch_dev, oracle_lib, bits):
+    """pmp_stream_update over random cuts (tiny, block-straddling, multi-node,
+    misaligned) gives the digest of pmp_hash_long / the oracle on the whole."""
+    import torch
+
+    cb = 128 * bits // 8
+    rng = random.Random(bits)
+    keys = pmp.Keys.generate(90, bits)
+    ok = oracle_lib.keygen(90, bits)
+    for total in [0, 1, 7, cb - 1, cb, cb + 1, 3 * cb + 5, 128 * cb, 128 * cb + 1, 300 * cb + 77,
+                  128 * 128 * cb + 3 * cb + 9]:
+        data = datagen.payload_host(91 + total % 7, 0, total)
+        d = torch.from_numpy(data if total else np.zeros(1, np.uint8)).to(torch_dev)
+        want = oracle_lib.hash_long(ok, data, nthreads=NT)
+        for trial in range(3):
+            st = pmp.Stream(keys)
+            pos = 0
+            while pos < total:
+                kind = rng.random()
+                step = rng.randrange(1, 17) if kind < 0.4 else (rng.randrange(1, 3 * cb) if kind < 0.8
+                                                               else rng.randrange(1, 300 * cb))
+                step = min(step, total - pos)
+                st.update(d[pos:], step)
+                pos += step
+            got = int(pmp.as_u64(st.final())[0])
+            assert got == want, (total, trial)
+            st.close()
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_stream_large_pieces(torch_dev, oracle_lib, bits):
+    """Pieces of 2-40 MiB (hundreds of level-2 nodes per update, so fewer
+    pieces per node in k_node and many nodes completing inside one merge),
+    with level-3 nodes closing mid-update, against the oracle."""
+    import torch
+
+    cb = 128 * bits // 8
+    total = 3 * 128 * 128 * cb + 5 * cb + 3
+    data = datagen.payload_host(95 + bits, 0, total)
+    d = torch.from_numpy(data).to(torch_dev)
+    keys = pmp.Keys.generate(94, bits)
+    want = oracle_lib.hash_long(oracle_lib.keygen(94, bits), data, nthreads=NT)
+    for cuts in ([total], [total // 3 + 17, total // 2 + 1000], [2 * 128 * 128 * cb - 1, 1, 5 << 20]):
+        st = pmp.Stream(keys)
+        pos = 0
+        for c in cuts + [total - sum(cuts)]:
+            if c:
+                st.update(d[pos:], c)
+            pos += c
+        assert int(pmp.as_u64(st.final())[0]) == want, cuts
+        st.close()
+
+
+def test_stream_reset_and_reuse(torch_dev, oracle_lib):
+    import torch
+
+    keys = pmp.Keys.generate(92, 64)
+    st = pmp.Stream(keys)
+    for total in (5000, 17, 0):
+        data = datagen.payload_host(93, 0, total)
+        d = torch.from_numpy(data if total else np.zeros(1, np.uint8)).to(torch_dev)
+        if total:
+            st.update(d, total)
+        got = int(pmp.as_u64(st.final())[0])
+        assert got == oracle_lib.hash_long(oracle_lib.keygen(92, 64), data)
+        with pytest.raises(pmp.PmpError):
+            st.update(d, 1)
+        st.reset()
