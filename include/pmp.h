@@ -45,6 +45,9 @@ struct CUstream_st; /* = cudaStream_t */
 #define PMP_ECUDA (-3)    /* CUDA runtime error at launch / allocation */
 #define PMP_ENOMEM (-4)   /* host or device allocation failure */
 #define PMP_ENODEV (-5)   /* no CUDA device, or the key handle has no device copy */
+#define PMP_EBADFILE (-6) /* KeyFile: wrong magic or wrong length (SPEC "BadMagic") */
+#define PMP_EVERSION (-7) /* KeyFile: unsupported version, word size or level count */
+#define PMP_EKEYRANGE (-8) /* KeyFile: a key outside its range (SPEC "KeyOutOfRange") */
 
 /* Opaque key schedule: b_j and a_{j,1..128} for j = 1..8 (Alg. 1 REQUIRE,
  * P:431; Eq. (1)).  Immutable after creation; may be shared by any
@@ -71,6 +74,25 @@ int pmp_keys_export(const pmp_keys *keys, uint64_t *b, uint64_t *a);
 
 /* 32 or 64, or PMP_EINVAL for NULL. */
 int pmp_keys_bits(const pmp_keys *keys);
+
+/* KeyFile (layout SPEC S:289-295, "invented artifact plumbing"):
+ *   bytes 0-3 "PMPH", 4 version = 0x01, 5 word size in bits (0x20 | 0x40),
+ *   6 levels = 0x08, 7 reserved = 0x00, then for j = 1..8: b_j followed by
+ *   a_{j,1..128}, each a little-endian word of n/8 bytes.
+ * pmp_keyfile_size: 8 + 8 * 129 * n/8 = 8264 (64-bit) / 4136 (32-bit) bytes,
+ *   0 for a bad width.
+ * pmp_keys_save: serialise `keys` into the host buffer out[cap]; returns 0, or
+ *   PMP_EINVAL for NULL or cap < pmp_keyfile_size.
+ * pmp_keys_load: parse a host buffer buf[len] and upload the schedule as
+ *   pmp_keys_from_words does.  Validates the magic and exact length
+ *   (PMP_EBADFILE), version / word size / level count / reserved byte
+ *   (PMP_EVERSION), and every key range, b_j < 2^n and 1 <= a <= p - kappa - 1
+ *   (PMP_EKEYRANGE).  Returns the handle, or NULL with *err (if err != NULL)
+ *   set to the code; *err = 0 on success.  load(save(k)) exports the same
+ *   words as k. */
+uint64_t pmp_keyfile_size(int out_bits);
+int pmp_keys_save(const pmp_keys *keys, uint8_t *out, uint64_t cap);
+pmp_keys *pmp_keys_load(const uint8_t *buf, uint64_t len, int *err);
 
 void pmp_keys_free(pmp_keys *keys);
 

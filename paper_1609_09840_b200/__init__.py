@@ -19,6 +19,7 @@ from . import _build
 LIB_PATH = _build.LIB
 
 PMP_OK, PMP_EINVAL, PMP_ETOOLONG, PMP_ECUDA, PMP_ENOMEM, PMP_ENODEV = 0, -1, -2, -3, -4, -5
+PMP_EBADFILE, PMP_EVERSION, PMP_EKEYRANGE = -6, -7, -8
 
 _u64, _vp, _int = ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int
 _lib = None
@@ -42,6 +43,9 @@ def lib() -> ctypes.CDLL:
             "pmp_keys_from_words": ([_int, _vp, _vp], _vp),
             "pmp_keys_export": ([_vp, _vp, _vp], _int),
             "pmp_keys_bits": ([_vp], _int),
+            "pmp_keyfile_size": ([_int], _u64),
+            "pmp_keys_save": ([_vp, _vp, _u64], _int),
+            "pmp_keys_load": ([_vp, _u64, ctypes.POINTER(_int)], _vp),
             "pmp_keys_free": ([_vp], None),
             "pmp_hash_batch": ([_vp, _vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_batch_buckets": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _vp, _vp], _int),
@@ -90,6 +94,21 @@ def pmp_keys_from_words(out_bits: int, b_ptr: int, a_ptr: int) -> int:
 
 def pmp_keys_export(keys: int, b_ptr: int, a_ptr: int) -> int:
     return lib().pmp_keys_export(keys, b_ptr, a_ptr)
+
+
+def pmp_keyfile_size(out_bits: int) -> int:
+    return int(lib().pmp_keyfile_size(out_bits))
+
+
+def pmp_keys_save(keys: int, out_ptr: int, cap: int) -> int:
+    return lib().pmp_keys_save(keys, out_ptr, cap)
+
+
+def pmp_keys_load(buf_ptr: int, length: int) -> tuple[int, int]:
+    """Returns (handle or 0, error code)."""
+    err = _int(0)
+    h = lib().pmp_keys_load(buf_ptr, length, ctypes.byref(err)) or 0
+    return h, err.value
 
 
 def pmp_keys_free(keys: int) -> None:
@@ -191,6 +210,21 @@ class Keys:
         a = np.ascontiguousarray(a, dtype=np.uint64).reshape(-1)
         assert b.size == 8 and a.size == 8 * 128
         return cls(pmp_keys_from_words(bits, b.ctypes.data, a.ctypes.data), bits)
+
+    def save(self) -> bytes:
+        """The KeyFile bytes."""
+        n = pmp_keyfile_size(self.bits)
+        buf = ctypes.create_string_buffer(n)
+        _check(pmp_keys_save(self.handle, ctypes.addressof(buf), n), "pmp_keys_save")
+        return buf.raw
+
+    @classmethod
+    def load(cls, data: bytes) -> "Keys":
+        buf = ctypes.create_string_buffer(bytes(data), len(data))
+        h, err = pmp_keys_load(ctypes.addressof(buf), len(data))
+        if not h:
+            raise PmpError(err, "pmp_keys_load")
+        return cls(h, lib().pmp_keys_bits(h))
 
     def export(self):
         import numpy as np

@@ -192,7 +192,9 @@ u128 long_constant(const pmp_keys *k, uint64_t len) {
 }
 
 const char *kErr[] = {"ok", "invalid argument", "string too long (> 2^56-1 words)", "CUDA error",
-                      "out of memory", "no CUDA device for this key handle"};
+                      "out of memory", "no CUDA device for this key handle",
+                      "bad key file (magic or length)", "unsupported key file version, word size or levels",
+                      "key out of range"};
 
 struct Scratch {
   void *p = nullptr;
@@ -438,7 +440,7 @@ void pmp_stream_free(pmp_stream *s) {
 
 
 const char *pmp_strerror(int code) {
-  if (code > 0 || code < -5) return "unknown error";
+  if (code > 0 || code < -8) return "unknown error";
   return kErr[-code];
 }
 
@@ -497,6 +499,77 @@ int pmp_keys_export(const pmp_keys *k, uint64_t *b, uint64_t *a) {
 }
 
 int pmp_keys_bits(const pmp_keys *k) { return k ? k->bits : PMP_EINVAL; }
+
+uint64_t pmp_keyfile_size(int out_bits) {
+  if (out_bits != 32 && out_bits != 64) return 0;
+  return 8 + (uint64_t)kL * (1 + kM) * (out_bits / 8);
+}
+
+int pmp_keys_save(const pmp_keys *k, uint8_t *out, uint64_t cap) {
+  if (!k || !out || cap < pmp_keyfile_size(k->bits)) return PMP_EINVAL;
+  const int w = k->bits / 8;
+  memcpy(out, "PMPH", 4);
+  out[4] = 0x01;
+  out[5] = (uint8_t)k->bits;
+  out[6] = (uint8_t)kL;
+  out[7] = 0x00;
+  uint8_t *p = out + 8;
+  auto put = [&](uint64_t x) {
+    for (int i = 0; i < w; i++) *p++ = (uint8_t)(x >> (8 * i));
+  };
+  for (uint32_t j = 0; j < kL; j++) {
+    put(k->b[j]);
+    for (uint32_t i = 0; i < kM; i++) put(k->a[j * kM + i]);
+  }
+  return 0;
+}
+
+pmp_keys *pmp_keys_load(const uint8_t *buf, uint64_t len, int *err) {
+  int e = 0;
+  if (!err) err = &e;
+  *err = PMP_EINVAL;
+  if (!buf) return nullptr;
+  *err = PMP_EBADFILE;
+  if (len < 8 || memcmp(buf, "PMPH", 4) != 0) return nullptr;
+  const int bits = buf[5];
+  *err = PMP_EVERSION;
+  if (buf[4] != 0x01 || (bits != 32 && bits != 64) || buf[6] != kL || buf[7] != 0x00) return nullptr;
+  *err = PMP_EBADFILE;
+  if (len != pmp_keyfile_size(bits)) return nullptr;
+  const int w = bits / 8;
+  const uint8_t *p = buf + 8;
+  auto get = [&]() {
+    uint64_t x = 0;
+    for (int i = 0; i < w; i++) x |= (uint64_t)*p++ << (8 * i);
+    return x;
+  };
+  pmp_keys *k = new (std::nothrow) pmp_keys;
+  *err = PMP_ENOMEM;
+  if (!k) return nullptr;
+  k->bits = bits;
+  k->device = -1;
+  k->d_blob = nullptr;
+  const uint64_t amax = amax_of(bits);
+  for (uint32_t j = 0; j < kL; j++) {
+    k->b[j] = get();  // a w-byte word is < 2^n by construction
+    for (uint32_t i = 0; i < kM; i++) {
+      const uint64_t a = get();
+      if (a == 0 || a > amax) {
+        delete k;
+        *err = PMP_EKEYRANGE;
+        return nullptr;
+      }
+      k->a[j * kM + i] = a;
+    }
+  }
+  if (upload(k) != 0) {
+    delete k;
+    *err = PMP_ENOMEM;
+    return nullptr;
+  }
+  *err = 0;
+  return k;
+}
 
 void pmp_keys_free(pmp_keys *k) {
   if (!k) return;

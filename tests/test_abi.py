@@ -128,3 +128,55 @@ def test_long_constant_matches_oracle_tree_of_zero_blocks(L, oracle_lib, bits, l
 def test_bucket_call_rejects_zero_modulus(L):
     k = pmp.Keys.generate(1, 64)
     assert pmp.pmp_hash_batch_buckets(k.handle, 8, 8, 1, 0, 8, 0, 0) == pmp.PMP_EINVAL
+
+
+@pytest.mark.parametrize("bits,size", [(64, 8264), (32, 4136)])
+def test_keyfile_roundtrip_and_layout(L, bits, size):
+    """KeyFile: exact size, header bytes, and the
+    payload parsed here independently (b_j then a_{j,1..128}, LE n/8-byte
+    words) equals the schedule; load(save(k)) exports the same words."""
+    assert pmp.pmp_keyfile_size(bits) == size and pmp.pmp_keyfile_size(48) == 0
+    k = pmp.Keys.generate(77, bits)
+    raw = k.save()
+    assert len(raw) == size
+    assert raw[:4] == b"PMPH" and raw[4] == 1 and raw[5] == bits and raw[6] == 8 and raw[7] == 0
+    words = np.frombuffer(raw[8:], dtype="<u8" if bits == 64 else "<u4").astype(np.uint64).reshape(8, 129)
+    b, a = k.export()
+    assert np.array_equal(words[:, 0], b) and np.array_equal(words[:, 1:], a)
+    k2 = pmp.Keys.load(raw)
+    assert k2.bits == bits
+    b2, a2 = k2.export()
+    assert np.array_equal(b2, b) and np.array_equal(a2, a)
+    assert k2.save() == raw
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_keyfile_rejects_corrupt_files(L, bits):
+    raw = bytearray(pmp.Keys.generate(78, bits).save())
+    w = bits // 8
+    amax = 2**64 - 12 if bits == 64 else 2**32 - 14
+
+    def err(buf):
+        with pytest.raises(pmp.PmpError) as e:
+            pmp.Keys.load(bytes(buf))
+        return e.value.code
+
+    bad = bytearray(raw); bad[0:4] = b"PMPX"
+    assert err(bad) == pmp.PMP_EBADFILE
+    assert err(raw[:-1]) == pmp.PMP_EBADFILE            # truncated
+    assert err(raw + b"\0") == pmp.PMP_EBADFILE         # trailing bytes
+    assert err(raw[:3]) == pmp.PMP_EBADFILE
+    for pos, val in ((4, 2), (5, 0x30), (5, 96 - bits), (6, 7), (7, 1)):
+        bad = bytearray(raw); bad[pos] = val
+        assert err(bad) == (pmp.PMP_EVERSION if not (pos == 5 and val == 96 - bits) else pmp.PMP_EBADFILE)
+    for level, idx, val in ((0, 1, 0), (7, 128, 0), (3, 5, amax + 1), (5, 77, 2**bits - 1)):
+        bad = bytearray(raw)
+        o = 8 + (level * 129 + idx) * w
+        bad[o:o + w] = val.to_bytes(w, "little")
+        assert err(bad) == pmp.PMP_EKEYRANGE, (level, idx, val)
+    ok = bytearray(raw)                                  # boundary values are legal
+    for level, idx, val in ((2, 1, 1), (2, 2, amax), (4, 0, 2**bits - 1)):
+        o = 8 + (level * 129 + idx) * w
+        ok[o:o + w] = val.to_bytes(w, "little")
+    pmp.Keys.load(bytes(ok))
+    assert pmp.strerror(pmp.PMP_EKEYRANGE) == "key out of range"

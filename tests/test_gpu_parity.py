@@ -142,6 +142,17 @@ def test_tiny_config_every_hash(torch_dev, oracle_lib, bits):
 
 
 @pytest.mark.parametrize("bits", [32, 64])
+def test_keyfile_schedule_hashes_like_generated(torch_dev, oracle_lib, bits):
+    """A schedule round-tripped through the KeyFile (8(f3)) is uploaded and used
+    by the kernels exactly like the generated one: configs[0] against the oracle."""
+    wl = datagen.WORKLOADS["tiny"]
+    off = datagen.offsets_from_lengths(wl.lengths())
+    pay = datagen.payload_host(wl.seed, 0, int(off[-1]))
+    keys = pmp.Keys.load(pmp.Keys.generate(wl.seed, bits).save())
+    assert np.array_equal(run_batch(torch_dev, keys, pay, off), oracle_batch(oracle_lib, wl.seed, bits, pay, off))
+
+
+@pytest.mark.parametrize("bits", [32, 64])
 @pytest.mark.parametrize("shift", [0, 1, 3, 8, 13])
 def test_length_sweep_all_paths(torch_dev, oracle_lib, bits, shift):
     """Every length 0..2100 (short path <= 127 B, warp path beyond, 1..3 level-1
