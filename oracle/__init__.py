@@ -72,6 +72,14 @@ def lib():
         h.pmpo_hash_batch.restype = None
         h.pmpo_hash_long.argtypes = [ctypes.c_int, _p, _p, _p, _u64, ctypes.c_int]
         h.pmpo_hash_long.restype = _u64
+        h.pmpo_hash2_value.argtypes = [ctypes.c_int, _p, _p, _p, _u64, ctypes.c_int, _p]
+        h.pmpo_hash2_value.restype = ctypes.c_int
+        h.pmpo_hash2.argtypes = [ctypes.c_int, _p, _p, _p, _u64, ctypes.c_int]
+        h.pmpo_hash2.restype = _u64
+        h.pmpo_hash2_batch.argtypes = [ctypes.c_int, _p, _p, _p, _p, _u64, _p, ctypes.c_int]
+        h.pmpo_hash2_batch.restype = None
+        h.pmpo_mulmod.argtypes = [_u64, _u64, _u64, _u64, _u64, _u64, _p]
+        h.pmpo_mulmod.restype = None
         _lib = h
     return _lib
 
@@ -202,4 +210,36 @@ def hash_batch(keys: Keys, payload: np.ndarray, offsets: np.ndarray, nthreads: i
     if n > 0:
         lib().pmpo_hash_batch(keys.bits, _ptr(keys.b), _ptr(keys.a), _ptr(payload),
                               _ptr(offsets), n, _ptr(out), nthreads)
+    return out
+
+
+# ---- two-level variant (reading Q19)
+def mulmod(p: int, x: int, y: int) -> int:
+    out = np.zeros(2, dtype=np.uint64)
+    M = 2**64 - 1
+    lib().pmpo_mulmod(p & M, p >> 64, x & M, x >> 64, y & M, y >> 64, _ptr(out))
+    return int(out[0]) | (int(out[1]) << 64)
+
+
+def hash2_value(keys: Keys, data, nthreads: int = 1) -> int:
+    arr = _bytes_arr(data)
+    out = np.zeros(2, dtype=np.uint64)
+    rc = lib().pmpo_hash2_value(keys.bits, _ptr(keys.b), _ptr(keys.a), _ptr(arr), arr.size, nthreads, _ptr(out))
+    assert rc == 0
+    return int(out[0]) | (int(out[1]) << 64)
+
+
+def hash2(keys: Keys, data, nthreads: int = 1) -> int:
+    arr = _bytes_arr(data)
+    return int(lib().pmpo_hash2(keys.bits, _ptr(keys.b), _ptr(keys.a), _ptr(arr), arr.size, nthreads))
+
+
+def hash2_batch(keys: Keys, payload: np.ndarray, offsets: np.ndarray, nthreads: int = 1) -> np.ndarray:
+    payload = np.ascontiguousarray(payload, dtype=np.uint8)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    n = offsets.size - 1
+    out = np.zeros(max(n, 0), dtype=np.uint64)
+    if n > 0:
+        lib().pmpo_hash2_batch(keys.bits, _ptr(keys.b), _ptr(keys.a), _ptr(payload), _ptr(offsets), n,
+                               _ptr(out), nthreads)
     return out

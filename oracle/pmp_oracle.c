@@ -346,3 +346,120 @@ void pmpo_hash_batch(int bits, const uint64_t *b, const uint64_t *a,
   free(jobs);
   free(th);
 }
+
+/* ---- Two-level variant (reading Q19 in DESIGN.md) ----
+ * "only the first level uses Multilinear, while the second level uses a
+ * polynomial hash family":
+ *   v_c = f_1(chunk c)            c = 0 .. C-1, C = ceil(T / 128) (Eq. (1), as the tree)
+ *   h = 0; for c: h = (h + v_c) * r mod p      (Horner: h = sum_c v_c r^(C-c))
+ *   V = (h + beta) mod p,  r = a_{2,1}, beta = b_2 (keys of the same schedule)
+ *   digest = mix(V mod 2^n).
+ * Every string, including T == 1, goes through both levels. */
+
+/* x * y mod p for x, y < p < 2^66: shift-and-add over the bits of y (every
+ * intermediate < 2p < 2^67). */
+static u128 mulmod_u128(u128 x, u128 y, u128 p) {
+  u128 r = 0;
+  for (int i = 127; i >= 0; i--) {
+    r = (r << 1) % p;
+    if ((y >> i) & 1) r = (r + x) % p;
+  }
+  return r;
+}
+
+void pmpo_mulmod(uint64_t p_lo, uint64_t p_hi, uint64_t x_lo, uint64_t x_hi,
+                 uint64_t y_lo, uint64_t y_hi, uint64_t *out) {
+  u128 r = mulmod_u128(mk(x_lo, x_hi), mk(y_lo, y_hi), mk(p_lo, p_hi));
+  out[0] = (uint64_t)r;
+  out[1] = (uint64_t)(r >> 64);
+}
+
+static int hash2_value_u128(int bits, const uint64_t *b, const uint64_t *a,
+                            const uint8_t *bytes, uint64_t len, int nthreads, u128 *V) {
+  uint64_t plo, phi;
+  if (pmpo_params(bits, &plo, &phi, NULL, NULL, NULL) != 0) return -1;
+  u128 p = mk(plo, phi);
+  uint64_t T = pmpo_num_words(bits, len);
+  uint64_t C = (T + PMPO_M - 1) / PMPO_M; /* chunks, last one zero-padded */
+  u128 *y = (u128 *)malloc(sizeof(u128) * (size_t)C);
+  if (nthreads < 1) nthreads = 1;
+  if ((uint64_t)nthreads > C) nthreads = (int)C;
+  l1_job *jobs = (l1_job *)calloc((size_t)nthreads, sizeof(l1_job));
+  pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+  for (int i = 0; i < nthreads; i++) {
+    l1_job *jb = &jobs[i];
+    jb->bits = bits; jb->p = p; jb->b = b; jb->a = a;
+    jb->bytes = bytes; jb->len = len; jb->T = T; jb->y = y;
+    jb->c_begin = C * (uint64_t)i / (uint64_t)nthreads;
+    jb->c_end = C * (uint64_t)(i + 1) / (uint64_t)nthreads;
+    if (nthreads == 1) l1_worker(jb);
+    else pthread_create(&th[i], NULL, l1_worker, jb);
+  }
+  if (nthreads > 1)
+    for (int i = 0; i < nthreads; i++) pthread_join(th[i], NULL);
+  free(jobs);
+  free(th);
+  const u128 r = a[PMPO_M]; /* a_{2,1} */
+  const u128 beta = b[1];   /* b_2 */
+  u128 h = 0;
+  for (uint64_t c = 0; c < C; c++) h = mulmod_u128((h + y[c]) % p, r, p);
+  free(y);
+  *V = (h + beta) % p;
+  return 0;
+}
+
+int pmpo_hash2_value(int bits, const uint64_t *b, const uint64_t *a,
+                     const uint8_t *bytes, uint64_t len, int nthreads, uint64_t *out) {
+  u128 V = 0;
+  int rc = hash2_value_u128(bits, b, a, bytes, len, nthreads, &V);
+  out[0] = (uint64_t)V;
+  out[1] = (uint64_t)(V >> 64);
+  return rc;
+}
+
+uint64_t pmpo_hash2(int bits, const uint64_t *b, const uint64_t *a,
+                    const uint8_t *bytes, uint64_t len, int nthreads) {
+  u128 V = 0;
+  hash2_value_u128(bits, b, a, bytes, len, nthreads, &V);
+  return digest_of(bits, V);
+}
+
+typedef struct {
+  int bits;
+  const uint64_t *b, *a, *offsets;
+  const uint8_t *bytes;
+  uint64_t i0, i1;
+  uint64_t *out;
+} batch2_job;
+
+static void *batch2_worker(void *arg) {
+  batch2_job *jb = (batch2_job *)arg;
+  for (uint64_t i = jb->i0; i < jb->i1; i++) {
+    uint64_t o0 = jb->offsets[i], o1 = jb->offsets[i + 1];
+    jb->out[i] = pmpo_hash2(jb->bits, jb->b, jb->a, jb->bytes + o0, o1 - o0, 1);
+  }
+  return NULL;
+}
+
+void pmpo_hash2_batch(int bits, const uint64_t *b, const uint64_t *a,
+                      const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
+                      uint64_t *out, int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  if (n == 0) return;
+  if ((uint64_t)nthreads > n) nthreads = (int)n;
+  batch2_job *jobs = (batch2_job *)calloc((size_t)nthreads, sizeof(batch2_job));
+  pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+  for (int i = 0; i < nthreads; i++) {
+    batch2_job *jb = &jobs[i];
+    jb->bits = bits; jb->b = b; jb->a = a; jb->offsets = offsets;
+    jb->bytes = bytes; jb->out = out;
+    jb->i0 = n * (uint64_t)i / (uint64_t)nthreads;
+    jb->i1 = n * (uint64_t)(i + 1) / (uint64_t)nthreads;
+    if (nthreads == 1) batch2_worker(jb);
+    else pthread_create(&th[i], NULL, batch2_worker, jb);
+  }
+  if (nthreads > 1)
+    for (int i = 0; i < nthreads; i++) pthread_join(th[i], NULL);
+  free(jobs);
+  free(th);
+}

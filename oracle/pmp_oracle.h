@@ -98,6 +98,23 @@ void pmpo_hash_batch(int bits, const uint64_t *b, const uint64_t *a,
 uint64_t pmpo_hash_long(int bits, const uint64_t *b, const uint64_t *a,
                         const uint8_t *bytes, uint64_t len, int nthreads);
 
+/* Two-level variant (reading Q19): level 1 = f_1 on each
+ * 128-word chunk (as the tree), level 2 = Horner polynomial in r = a_{2,1}
+ * over the C chunk values, V = (b_2 + sum_c v_c r^(C-c)) mod p, for every
+ * string (T == 1 included).  `nthreads` parallelises the level-1 map only. */
+int pmpo_hash2_value(int bits, const uint64_t *b, const uint64_t *a,
+                     const uint8_t *bytes, uint64_t len, int nthreads, uint64_t *out);
+uint64_t pmpo_hash2(int bits, const uint64_t *b, const uint64_t *a,
+                    const uint8_t *bytes, uint64_t len, int nthreads);
+
+void pmpo_hash2_batch(int bits, const uint64_t *b, const uint64_t *a,
+                      const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
+                      uint64_t *out, int nthreads);
+
+/* x * y mod p (x, y < p < 2^66) by shift-and-add; out = (lo, hi). */
+void pmpo_mulmod(uint64_t p_lo, uint64_t p_hi, uint64_t x_lo, uint64_t x_hi,
+                 uint64_t y_lo, uint64_t y_hi, uint64_t *out);
+
 #ifdef __cplusplus
 }
 #endif
