@@ -142,10 +142,11 @@ def make_batch(wl, rank, n=None):
     return seed, lens, offs, 0
 
 
-def oracle_sample_rate(wl, seed, offs, bits_list, budget_s=12.0, max_threads=None, base=0):
+def oracle_sample_rate(wl, seed, offs, bits_list, budget_s=12.0, max_threads=None, base=0, variant="tree"):
     """Oracle GB/s on a bounded prefix sample of the batch (all host threads)."""
     import oracle
 
+    hb = oracle.hash2_batch if variant == "two-level" else oracle.hash_batch
     threads = max_threads or os.cpu_count() or 1
     keys = {b: oracle.keygen(wl.seed, b) for b in bits_list}
     # calibrate on 2^15 strings, then size the sample to ~budget_s
@@ -155,26 +156,29 @@ def oracle_sample_rate(wl, seed, offs, bits_list, budget_s=12.0, max_threads=Non
     pay = datagen.payload_host(seed, base, int(offs[n_cal]))
     t0 = time.perf_counter()
     for b in bits_list:
-        oracle.hash_batch(keys[b], pay, offs[:n_cal + 1], nthreads=threads)
+        hb(keys[b], pay, offs[:n_cal + 1], nthreads=threads)
     dt = time.perf_counter() - t0
     n_s = int(min(offs.size - 1, max(n_cal, n_cal * budget_s / max(dt, 1e-6))))
     pay = datagen.payload_host(seed, base, int(offs[n_s]))
     t0 = time.perf_counter()
     for b in bits_list:
-        oracle.hash_batch(keys[b], pay, offs[:n_s + 1], nthreads=threads)
+        hb(keys[b], pay, offs[:n_s + 1], nthreads=threads)
     dt = time.perf_counter() - t0
     nbytes = int(offs[n_s]) * len(bits_list)
     return nbytes / dt / 1e9, threads, f"first {n_s} strings of the batch ({int(offs[n_s])} B), widths {bits_list}", dt
 
 
-def oracle_long_rate(wl, nbytes_sample, budget_s=12.0):
+def oracle_long_rate(wl, nbytes_sample, budget_s=12.0, variant="tree"):
     import oracle
 
     threads = os.cpu_count() or 1
     k = oracle.keygen(wl.seed, 64)
     pay = datagen.payload_host(wl.seed, 0, nbytes_sample)
     t0 = time.perf_counter()
-    oracle.hash_long(k, pay, nthreads=threads)
+    if variant == "two-level":
+        oracle.hash2(k, pay, nthreads=threads)
+    else:
+        oracle.hash_long(k, pay, nthreads=threads)
     dt = time.perf_counter() - t0
     return nbytes_sample / dt / 1e9, threads, f"first {nbytes_sample} B of the 16 GiB string hashed as one string", dt
 
@@ -189,14 +193,15 @@ def run_reference(args, wl):
     desc = cores = None
     if wl.long:
         for i in range(args.warmup + args.steps):
-            r, cores, desc, dt = oracle_long_rate(wl, 64 << 20)
+            r, cores, desc, dt = oracle_long_rate(wl, 64 << 20, variant=args.variant)
             if i >= args.warmup:
                 rates.append(r)
                 times.append(dt)
     else:
         seed, lens, offs, b0 = make_batch(wl, 0, n=min(wl.n, 1 << 22))
         for i in range(args.warmup + args.steps):
-            r, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=4.0, base=b0)
+            r, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=4.0, base=b0,
+                                                    variant=args.variant)
             if i >= args.warmup:
                 rates.append(r)
                 times.append(dt)
@@ -205,14 +210,14 @@ def run_reference(args, wl):
             "value": v, "unit": unit, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * statistics.median(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64+u32" if len(wl.bits) > 1 else f"u{wl.bits[0]}",
-            "data": "synthetic (seeded xoshiro256** bytes)", "config": workload_config(wl, args.gpus),
+            "data": "synthetic (seeded xoshiro256** bytes)", "config": workload_config(wl, args.gpus, args.variant),
             "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(wl, gpus):
+def workload_config(wl, gpus, variant="tree"):
     c = {"workload": wl.name, "strings_per_gpu": wl.n if wl.name != "mixed" else "shard of 8 (~2^19)",
          "len_bytes": [wl.lo, wl.hi],
          "len_dist": {0: "fixed", 1: "uniform", 2: "log-uniform"}[wl.kind], "bits": list(wl.bits),
@@ -221,6 +226,8 @@ def workload_config(wl, gpus):
     if wl.long:
         c["strings_per_gpu"] = None
         c["string_bytes"] = wl.lo
+    if variant != "tree":
+        c["variant"] = "two-level: multilinear chunks + polynomial in r (8(f4), reading Q19)"
     return c
 
 
@@ -238,6 +245,8 @@ def main():
     ap.add_argument("--buckets", type=int, default=0,
                     help="hash-table consumer (SURVEY 8(f3)): write digest mod M + histogram instead of digests")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--variant", default="tree", choices=["tree", "two-level"],
+                    help="two-level: the multilinear + polynomial variant (8(f4), pmp_hash2_*)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -274,6 +283,8 @@ def main():
 
     keys = {b: pmp.Keys.generate(wl.seed, b) for b in wl.bits}
     outs = {}
+    v2 = args.variant == "two-level"
+    assert not (v2 and (args.buckets or args.stream_mib)), "--variant two-level: plain digests only"
     if wl.long:
         total = wl.lo
         begins = pmp.pmp_long_split(64, total, world)
@@ -301,8 +312,9 @@ def main():
             if args.stream_mib:
                 assert world == 1, "--stream-mib measures one GPU"
                 return step_stream()
-            pmp._check(pmp.pmp_hash_long_partial(keys[64].handle, d_full.data_ptr(), hi - lo, lo, total,
-                                                 parts[2 * rank:2 * rank + 2].data_ptr(), sp), "partial")
+            part_fn = pmp.pmp_hash2_long_partial if v2 else pmp.pmp_hash_long_partial
+            pmp._check(part_fn(keys[64].handle, d_full.data_ptr(), hi - lo, lo, total,
+                               parts[2 * rank:2 * rank + 2].data_ptr(), sp), "partial")
             if world > 1:
                 if backend == "nccl":
                     dist.all_gather_into_tensor(parts, parts[2 * rank:2 * rank + 2].clone())
@@ -310,9 +322,13 @@ def main():
                     host = parts.cpu()
                     dist.all_gather_into_tensor(host, host[2 * rank:2 * rank + 2].clone())
                     parts.copy_(host)
-            pmp._check(pmp.pmp_hash_long_combine(keys[64].handle, parts.data_ptr(), world, total,
-                                                 out.data_ptr(), sp), "combine")
-        dominant = "k_stream_node" if args.stream_mib else "k_node"
+            if v2:
+                pmp._check(pmp.pmp_hash2_long_combine(keys[64].handle, parts.data_ptr(), world, out.data_ptr(), sp),
+                           "combine")
+            else:
+                pmp._check(pmp.pmp_hash_long_combine(keys[64].handle, parts.data_ptr(), world, total,
+                                                     out.data_ptr(), sp), "combine")
+        dominant = "k_stream_node" if args.stream_mib else ("k_poly_node" if v2 else "k_node")
         alg_bytes_per_launch = min(piece, hi - lo) if args.stream_mib else hi - lo
         n = 1
     else:
@@ -337,9 +353,10 @@ def main():
                                                           args.buckets, outs[b].data_ptr(), counts.data_ptr(), sp),
                                "pmp_hash_batch_buckets")
                 else:
-                    pmp._check(pmp.pmp_hash_batch(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
-                                                  outs[b].data_ptr(), sp), "pmp_hash_batch")
-        dominant = "k_short" if wl.hi <= 127 else "k_wstring"
+                    fn = pmp.pmp_hash2_batch if v2 else pmp.pmp_hash_batch
+                    pmp._check(fn(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
+                                  outs[b].data_ptr(), sp), "pmp_hash_batch")
+        dominant = "k_short" if wl.hi <= 127 else ("k_poly_wstring" if v2 else "k_wstring")
         # algorithmic bytes per dominant launch: payload + offsets + digests (avg over widths)
         alg_bytes_per_launch = total_bytes + 8 * (n + 1) + n * sum(b // 8 for b in wl.bits) / len(wl.bits)
     torch.cuda.synchronize()
@@ -365,7 +382,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     k_ms, k_cnt = pmp.pmp_prof_read(dominant)
     kernel_ms = {name: pmp.pmp_prof_read(name) for name in ("k_short", "k_wstring", "k_node", "k_level", "k_combine",
-                                                             "k_stream")}
+                                                             "k_stream", "k_poly")}
     t = torch.tensor([ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -390,7 +407,7 @@ def main():
         clocks = clk.summary()
         cpu = None
         if not args.no_cpu:
-            cpu = cpu_baseline(wl)
+            cpu = cpu_baseline(wl, args.variant)
         line = {
             "metric": f"PM+ hashed GB/s ({'/'.join(str(b) for b in wl.bits)}-bit out)",
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -398,7 +415,7 @@ def main():
             "scaling": "strong" if wl.long else "weak", "vs_baseline": None,
             "dtype": "u64+u32" if len(wl.bits) > 1 else f"u{wl.bits[0]}",
             "data": "synthetic (seeded xoshiro256** bytes, generated on device)",
-            "config": dict(workload_config(wl, world), **({"output": f"buckets mod {args.buckets} + histogram"}
+            "config": dict(workload_config(wl, world, args.variant), **({"output": f"buckets mod {args.buckets} + histogram"}
                                                           if args.buckets else {}),
                            **({"api": f"pmp_stream_update in {args.stream_mib} MiB pieces"} if args.stream_mib else {})),
             "bytes_per_gpu_cycle": (value / world * 1e9) / (clocks["sm_mhz"] * 1e6) if clocks.get("sm_mhz") else None,
@@ -445,8 +462,9 @@ def run_e2e(args, wl, pmp, keys, dev, stream, rank, world, cdev):
         d_pay[:total].copy_(h_pay, non_blocking=True)
         d_off.copy_(h_off, non_blocking=True)
         for b in wl.bits:
-            pmp._check(pmp.pmp_hash_batch(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
-                                          d_out[b].data_ptr(), sp), "e2e hash")
+            fn = pmp.pmp_hash2_batch if args.variant == "two-level" else pmp.pmp_hash_batch
+            pmp._check(fn(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n, d_out[b].data_ptr(), sp),
+                       "e2e hash")
             h_out[b].copy_(d_out[b], non_blocking=True)
 
     step()
@@ -470,13 +488,14 @@ def run_e2e(args, wl, pmp, keys, dev, stream, rank, world, cdev):
             "path": "pinned host -> cudaMemcpyAsync -> pmp_hash_batch (both widths) -> host"}
 
 
-def cpu_baseline(wl):
+def cpu_baseline(wl, variant="tree"):
     try:
         if wl.long:
-            v, cores, desc, dt = oracle_long_rate(wl, 256 << 20)
+            v, cores, desc, dt = oracle_long_rate(wl, 256 << 20, variant=variant)
         else:
             seed, lens, offs, b0 = make_batch(wl, 0, n=min(wl.n, 1 << 23))
-            v, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=10.0, base=b0)
+            v, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=10.0, base=b0,
+                                                    variant=variant)
         return {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc,
                 "seconds": dt}
     except Exception as e:  # pragma: no cover

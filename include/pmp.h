@@ -168,6 +168,31 @@ int pmp_stream_final(pmp_stream *s, void *out, struct CUstream_st *stream);
 int pmp_stream_reset(pmp_stream *s, struct CUstream_st *stream);
 void pmp_stream_free(pmp_stream *s);
 
+/* ---- Two-level variant ("a two-level approach where
+ * only the first level uses Multilinear, while the second level uses a
+ * polynomial hash family"; the formula is reading Q19 in DESIGN.md):
+ *   v_c = f_1(chunk c) = (b_1 + sum_i a_{1,i} sigma_{128c+i}) mod p, c < C = ceil(T/128)
+ *   V   = (b_2 + sum_{c<C} v_c r^(C-c)) mod p,   r = a_{2,1}
+ *   digest = mix(V mod 2^n)   -- for every string, T == 1 included.
+ * It uses the same key schedule (keygen / KeyFile) and produces different
+ * digests from the tree.  Conventions, arguments and errors are those of the
+ * tree calls of the same shape:
+ *   pmp_hash2_batch        ~ pmp_hash_batch
+ *   pmp_hash2_long         ~ pmp_hash_long
+ *   pmp_hash2_long_partial ~ pmp_hash_long_partial: the caller's chunks
+ *       contribute sum v_c r^(C-c) (a field element, 2 words) -- no key-only
+ *       constant is needed, the sum is linear in the v_c;
+ *   pmp_hash2_long_combine: digest of b_2 + sum_g P_g (G partials, device). */
+int pmp_hash2_batch(const pmp_keys *keys, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
+                    void *out, struct CUstream_st *stream);
+int pmp_hash2_long(const pmp_keys *keys, const uint8_t *bytes, uint64_t len, void *out,
+                   struct CUstream_st *stream);
+int pmp_hash2_long_partial(const pmp_keys *keys, const uint8_t *local, uint64_t local_len,
+                           uint64_t global_offset, uint64_t total_len, uint64_t *partial,
+                           struct CUstream_st *stream);
+int pmp_hash2_long_combine(const pmp_keys *keys, const uint64_t *partials, int G, void *out,
+                           struct CUstream_st *stream);
+
 /* Host-only helper: split [0, total_len) into G contiguous ranges aligned to
  * level-1 blocks with equal block counts (+- 1); begins[0..G] (host),
  * begins[G] = total_len.  Returns 0 or PMP_EINVAL. */

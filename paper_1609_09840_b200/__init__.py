@@ -53,6 +53,10 @@ def lib() -> ctypes.CDLL:
             "pmp_hash_long_partial": ([_vp, _vp, _u64, _u64, _u64, _vp, _vp], _int),
             "pmp_hash_long_combine": ([_vp, _vp, _int, _u64, _vp, _vp], _int),
             "pmp_long_split": ([_int, _u64, _int, _vp], _int),
+            "pmp_hash2_batch": ([_vp, _vp, _vp, _u64, _vp, _vp], _int),
+            "pmp_hash2_long": ([_vp, _vp, _u64, _vp, _vp], _int),
+            "pmp_hash2_long_partial": ([_vp, _vp, _u64, _u64, _u64, _vp, _vp], _int),
+            "pmp_hash2_long_combine": ([_vp, _vp, _int, _vp, _vp], _int),
             "pmp_stream_new": ([_vp], _vp),
             "pmp_stream_update": ([_vp, _vp, _u64, _vp], _int),
             "pmp_stream_final": ([_vp, _vp, _vp], _int),
@@ -137,6 +141,24 @@ def pmp_hash_long_partial(keys: int, local_ptr: int, local_len: int, global_offs
 def pmp_hash_long_combine(keys: int, partials_ptr: int, G: int, total_len: int, out_ptr: int,
                           stream: int) -> int:
     return lib().pmp_hash_long_combine(keys, partials_ptr, G, total_len, out_ptr, stream)
+
+
+def pmp_hash2_batch(keys: int, bytes_ptr: int, offsets_ptr: int, n: int, out_ptr: int, stream: int) -> int:
+    return lib().pmp_hash2_batch(keys, bytes_ptr, offsets_ptr, n, out_ptr, stream)
+
+
+def pmp_hash2_long(keys: int, bytes_ptr: int, length: int, out_ptr: int, stream: int) -> int:
+    return lib().pmp_hash2_long(keys, bytes_ptr, length, out_ptr, stream)
+
+
+def pmp_hash2_long_partial(keys: int, local_ptr: int, local_len: int, global_offset: int,
+                           total_len: int, partial_ptr: int, stream: int) -> int:
+    return lib().pmp_hash2_long_partial(keys, local_ptr, local_len, global_offset, total_len,
+                                        partial_ptr, stream)
+
+
+def pmp_hash2_long_combine(keys: int, partials_ptr: int, G: int, out_ptr: int, stream: int) -> int:
+    return lib().pmp_hash2_long_combine(keys, partials_ptr, G, out_ptr, stream)
 
 
 def pmp_stream_new(keys: int) -> int:
@@ -312,6 +334,52 @@ def hash_long_combine(keys: Keys, partials, total_len: int, out=None, stream=Non
         out = torch.empty(1, dtype=torch.int64 if keys.bits == 64 else torch.int32, device=partials.device)
     _check(pmp_hash_long_combine(keys.handle, partials.data_ptr(), G, total_len, out.data_ptr(),
                                  _stream_ptr(stream)), "pmp_hash_long_combine")
+    return out
+
+
+def hash2_batch(keys: Keys, payload, offsets, out=None, stream=None):
+    """Two-level variant (8(f4)) of hash_batch."""
+    import torch
+
+    n = offsets.numel() - 1
+    if out is None:
+        out = torch.empty(max(n, 0), dtype=torch.int64 if keys.bits == 64 else torch.int32,
+                          device=offsets.device)
+    _check(pmp_hash2_batch(keys.handle, payload.data_ptr(), offsets.data_ptr(), max(n, 0),
+                           out.data_ptr(), _stream_ptr(stream)), "pmp_hash2_batch")
+    return out
+
+
+def hash2_long(keys: Keys, data, length: int | None = None, out=None, stream=None):
+    import torch
+
+    length = data.numel() if length is None else length
+    if out is None:
+        out = torch.empty(1, dtype=torch.int64 if keys.bits == 64 else torch.int32, device=data.device)
+    _check(pmp_hash2_long(keys.handle, data.data_ptr(), length, out.data_ptr(), _stream_ptr(stream)),
+           "pmp_hash2_long")
+    return out
+
+
+def hash2_long_partial(keys: Keys, local, local_len: int, global_offset: int, total_len: int,
+                       partial=None, stream=None):
+    import torch
+
+    if partial is None:
+        partial = torch.zeros(2, dtype=torch.int64, device=local.device)
+    _check(pmp_hash2_long_partial(keys.handle, local.data_ptr(), local_len, global_offset, total_len,
+                                  partial.data_ptr(), _stream_ptr(stream)), "pmp_hash2_long_partial")
+    return partial
+
+
+def hash2_long_combine(keys: Keys, partials, out=None, stream=None):
+    import torch
+
+    G = partials.numel() // 2
+    if out is None:
+        out = torch.empty(1, dtype=torch.int64 if keys.bits == 64 else torch.int32, device=partials.device)
+    _check(pmp_hash2_long_combine(keys.handle, partials.data_ptr(), G, out.data_ptr(), _stream_ptr(stream)),
+           "pmp_hash2_long_combine")
     return out
 
 

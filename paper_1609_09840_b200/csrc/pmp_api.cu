@@ -7,6 +7,7 @@
 // CPU fallback.
 #include "../../include/pmp.h"
 #include "pmp_kernels.cuh"
+#include "pmp_poly.cuh"
 
 #include <cuda_runtime.h>
 
@@ -69,11 +70,18 @@ int upload(pmp_keys *k) {
   }
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return PMP_ECUDA;
-  std::vector<uint64_t> blob(kL + kL * kM);
+  std::vector<uint64_t> blob(kBlobWords, 0);  // b, a, then the variant's power tables (pmp_poly.cuh)
   memcpy(blob.data(), k->b, sizeof(k->b));
   memcpy(blob.data() + kL, k->a, sizeof(k->a));
   if (cudaMalloc(&k->d_blob, blob.size() * 8) != cudaSuccess) return PMP_ENOMEM;
   if (cudaMemcpy(k->d_blob, blob.data(), blob.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(k->d_blob);
+    k->d_blob = nullptr;
+    return PMP_ECUDA;
+  }
+  if (k->bits == 64) k_poly_setup<64><<<1, 32>>>(k->d_blob);
+  else k_poly_setup<32><<<1, 32>>>(k->d_blob);
+  if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
     cudaFree(k->d_blob);
     k->d_blob = nullptr;
     return PMP_ECUDA;
@@ -162,6 +170,8 @@ ParamKeys param_keys(const pmp_keys *k) {
   ParamKeys pk;
   for (int i = 0; i < 32; i++) pk.a[i] = k->a[i];
   pk.b = k->b[0];
+  pk.r = k->a[kM];  // a_{2,1}
+  pk.b2 = k->b[1];
   return pk;
 }
 
@@ -274,6 +284,55 @@ int long_partial_impl(const pmp_keys *k, const uint8_t *local, uint64_t local_le
     if (rc) return rc;
   }
   return 0;
+}
+
+// Two-level variant (8(f4)): sum over the caller's chunks [cb, ce) of
+// v_c r^(C-c) (pmp_poly.cuh), into `dst` as a field element (final == 0) or,
+// with b_2 added, as the digest (final == 1).
+template <int BITS>
+int poly_long_impl(const pmp_keys *k, const uint8_t *local, uint64_t local_len, uint64_t g0, uint64_t total,
+                   int final, void *dst, cudaStream_t st) {
+  const uint64_t CB = (uint64_t)chunk_bytes(BITS);
+  const uint64_t C = (words_of(BITS, total) + 127) / 128;
+  StrView s;
+  s.base = local;
+  s.g0 = g0;
+  s.avail_end = g0 + local_len;
+  s.B = total;
+  s.delta = (uint32_t)((uintptr_t)local & 15);
+  const bool owns_tail = g0 + local_len == total;
+  const uint64_t cb = g0 / CB;
+  const uint64_t ce = owns_tail ? C : (g0 + local_len) / CB;
+  const int sms = sm_count(k->device);
+  uint64_t grid = 1;
+  if (ce > cb) {
+    const uint64_t d = (128 - C % 128) % 128;
+    const uint64_t nodes = (ce - 1 + d) / 128 - (cb + d) / 128 + 1;
+    grid = (nodes + kWWarps - 1) / kWWarps;
+    if (grid > (uint64_t)sms * 16) grid = (uint64_t)sms * 16;
+  }
+  Scratch sc(st);
+  if (sc.alloc(grid * 16)) return PMP_ENOMEM;
+  uint64_t *parts = (uint64_t *)sc.p;
+  int rc;
+  if (ce > cb) {
+    rc = launch("k_poly_node", st, [&] {
+      k_poly_node<BITS><<<(unsigned)grid, kWWarps * 32, 0, st>>>(k->d_blob, s, cb, ce, C, parts);
+    });
+  } else {
+    rc = cudaMemsetAsync(parts, 0, 16, st) == cudaSuccess ? 0 : PMP_ECUDA;
+  }
+  if (rc) return rc;
+  return launch("k_poly_sum", st, [&] { k_poly_sum<BITS><<<1, 256, 0, st>>>(k->d_blob, parts, grid, final, dst); });
+}
+
+int poly_args(const pmp_keys *k, const uint8_t *local, uint64_t local_len, uint64_t g0, uint64_t total) {
+  if (!k || (!local && local_len > 0)) return PMP_EINVAL;
+  if (words_of(k->bits, total) > (1ULL << 56)) return PMP_ETOOLONG;
+  const uint64_t CB = (uint64_t)chunk_bytes(k->bits);
+  if (g0 % CB != 0 || g0 + local_len > total || g0 + local_len < g0) return PMP_EINVAL;
+  if (g0 + local_len != total && local_len % CB != 0) return PMP_EINVAL;
+  return check_keys(k);
 }
 
 }  // namespace
@@ -578,7 +637,7 @@ void pmp_keys_free(pmp_keys *k) {
 }
 
 static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
-                           const OutSpec &os, cudaStream_t st) {
+                           const OutSpec &os, cudaStream_t st, bool v2 = false) {
   if (!k) return PMP_EINVAL;
   if (n == 0) return 0;
   if (!bytes || !offsets || !os.out || n >= (1ULL << 32)) return PMP_EINVAL;
@@ -595,6 +654,8 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   std::call_once(attr_once, [] {
     cudaFuncSetAttribute(k_short<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
     cudaFuncSetAttribute(k_short<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
+    cudaFuncSetAttribute(k_short<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
+    cudaFuncSetAttribute(k_short<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
   });
   // the offsets ring is fed by TMA bulk copies, which need 16-byte aligned sources
   if ((uintptr_t)offsets & 15) {
@@ -611,6 +672,17 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   if (grid > maxgrid) grid = maxgrid;
   const int threads = (kShortWarps + 1) * 32;  // + producer warp
   int rc;
+  if (v2) {  // two-level variant (8(f4)): short strings in k_short, the rest warp per string
+    if (k->bits == 64)
+      rc = launch("k_short", st, [&] { k_short<64, true><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
+    else
+      rc = launch("k_short", st, [&] { k_short<32, true><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
+    if (rc) return rc;
+    const unsigned pgrid = (unsigned)(sms * 16);
+    if (k->bits == 64)
+      return launch("k_poly_wstring", st, [&] { k_poly_wstring<64><<<pgrid, kWWarps * 32, 0, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
+    return launch("k_poly_wstring", st, [&] { k_poly_wstring<32><<<pgrid, kWWarps * 32, 0, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
+  }
   if (k->bits == 64)
     rc = launch("k_short", st, [&] { k_short<64><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
   else
@@ -681,6 +753,38 @@ int pmp_hash_long(const pmp_keys *k, const uint8_t *bytes, uint64_t len, void *o
   int rc = pmp_hash_long_partial(k, bytes, len, 0, len, partial, st);
   if (rc) return rc;
   return pmp_hash_long_combine(k, partial, 1, len, out, st);
+}
+
+int pmp_hash2_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n, void *out,
+                    cudaStream_t st) {
+  OutSpec os;
+  os.out = out;
+  os.M = 0;
+  os.counts = nullptr;
+  return hash_batch_impl(k, bytes, offsets, n, os, st, true);
+}
+
+int pmp_hash2_long(const pmp_keys *k, const uint8_t *bytes, uint64_t len, void *out, cudaStream_t st) {
+  if (!out) return PMP_EINVAL;
+  if (int rc = poly_args(k, bytes, len, 0, len)) return rc;
+  return k->bits == 64 ? poly_long_impl<64>(k, bytes, len, 0, len, 1, out, st)
+                       : poly_long_impl<32>(k, bytes, len, 0, len, 1, out, st);
+}
+
+int pmp_hash2_long_partial(const pmp_keys *k, const uint8_t *local, uint64_t local_len, uint64_t g0,
+                           uint64_t total, uint64_t *partial, cudaStream_t st) {
+  if (!partial) return PMP_EINVAL;
+  if (int rc = poly_args(k, local, local_len, g0, total)) return rc;
+  return k->bits == 64 ? poly_long_impl<64>(k, local, local_len, g0, total, 0, partial, st)
+                       : poly_long_impl<32>(k, local, local_len, g0, total, 0, partial, st);
+}
+
+int pmp_hash2_long_combine(const pmp_keys *k, const uint64_t *partials, int G, void *out, cudaStream_t st) {
+  if (!k || !partials || !out || G < 1) return PMP_EINVAL;
+  if (int rc = check_keys(k)) return rc;
+  if (k->bits == 64)
+    return launch("k_poly_sum", st, [&] { k_poly_sum<64><<<1, 256, 0, st>>>(k->d_blob, partials, (uint64_t)G, 1, out); });
+  return launch("k_poly_sum", st, [&] { k_poly_sum<32><<<1, 256, 0, st>>>(k->d_blob, partials, (uint64_t)G, 1, out); });
 }
 
 int pmp_long_split(int out_bits, uint64_t total, int G, uint64_t *begins) {

@@ -32,6 +32,7 @@ constexpr uint32_t FULL = 0xffffffffu;
 struct ParamKeys {
   uint64_t a[32];
   uint64_t b;
+  uint64_t r, b2;  // two-level variant (reading Q19): r = a_{2,1}, b_2
 };
 
 // ------------------------------------------------------------- helpers
@@ -109,6 +110,38 @@ PMP_DI Fe64 fe_shfl(const Fe64 &v, int lane) {
 PMP_DI uint64_t fe_shfl(uint64_t v, int lane) { return __shfl_sync(FULL, v, lane); }
 PMP_DI Fe64 fe_from_word(uint64_t w, Fe64 *) { Fe64 r; r.lo = w; r.hi = 0; return r; }
 PMP_DI uint64_t fe_from_word(uint64_t w, uint64_t *) { return w; }
+PMP_DI uint32_t fe_hi(const Fe64 &v) { return v.hi; }
+PMP_DI uint32_t fe_hi(uint64_t v) { return (uint32_t)(v >> 32); }
+// x += v * 2^n (field element v; exact, the accumulators have headroom)
+PMP_DI void acc_add_fe_shl(Acc5 &x, const Fe64 &v) {
+  Acc5 h = {0, 0, (uint32_t)v.lo, (uint32_t)(v.lo >> 32), v.hi};
+  acc5_add(x, h);
+}
+PMP_DI void acc_add_fe_shl(Acc3 &x, uint64_t v) {
+  Acc3 h = {0, (uint32_t)v, (uint32_t)(v >> 32)};
+  acc3_add(x, h);
+}
+// x += w * v for two field elements: (w mod 2^n) * v + [w >= 2^n] v 2^n (< 2^(2n+2))
+PMP_DI void acc_mac_fe_full(Acc5 &x, const Fe64 &w, const Fe64 &v) {
+  acc5_mac_fe(x, w.lo, v);
+  if (w.hi) acc_add_fe_shl(x, v);
+}
+PMP_DI void acc_mac_fe_full(Acc3 &x, uint64_t w, uint64_t v) {
+  acc3_mac_fe(x, (uint32_t)w, v);
+  if (w >> 32) acc_add_fe_shl(x, v);
+}
+// w * v mod p (P:659-709 reduction of the exact product)
+template <class Fe> PMP_DI Fe fe_mul(const Fe &w, const Fe &v) {
+  if constexpr (sizeof(Fe) == 8) {
+    Acc3 x = {0, 0, 0};
+    acc_mac_fe_full(x, w, v);
+    return reduce_acc3(x);
+  } else {
+    Acc5 x = {0, 0, 0, 0, 0};
+    acc_mac_fe_full(x, w, v);
+    return reduce_acc5(x);
+  }
+}
 
 PMP_DI void load_acc(const uint32_t *w, Acc5 &x) { x.c0 = w[0]; x.c1 = w[1]; x.c2 = w[2]; x.c3 = w[3]; x.c4 = w[4]; }
 PMP_DI void load_acc(const uint32_t *w, Acc3 &x) { x.c0 = w[0]; x.c1 = w[1]; x.c2 = w[2]; }
@@ -169,7 +202,9 @@ template <int BITS> PMP_DI void emit(const OutSpec &os, uint64_t i, uint64_t lo)
 // own full words multiplies zeros (a*0 adds nothing), so the multiply-adds are
 // never branched around.  The marker word is done once per lane with
 // its key read from shared memory.
-template <int BITS, class Fetch>
+// V2: the two-level variant (reading Q19): V = b_2 + r * v_0 with v_0 = f_1 of
+// the single chunk (no |sigma| = 1 shortcut).
+template <int BITS, bool V2, class Fetch>
 PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ skeys, uint32_t B, uint32_t sh,
                               int tfull_max, Fetch fetch) {
   if constexpr (BITS == 64) {
@@ -195,10 +230,17 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
     const uint32_t z0 = fetch(2 * tlast), z1 = fetch(2 * tlast + 1), z2 = fetch(2 * tlast + 2);
     uint64_t w = ((uint64_t)funnel(z1, z2, sh) << 32) | funnel(z0, z1, sh);
     w = (w & ((1ULL << (8 * r)) - 1)) | (1ULL << (8 * r));    // bytes || 0x01 || 0
-    if (tlast == 0) return w;                                  // |sigma| = 1: no f_j (reading Q2)
+    if (!V2 && tlast == 0) return w;                           // |sigma| = 1: no f_j (reading Q2)
     mac64(A, skeys[tlast], w);
     Acc5 x = macc_normalize(A);
     acc5_add_u64(x, K.b);
+    if constexpr (V2) {
+      const Fe64 v0 = reduce_acc5(x);
+      Acc5 y = {0, 0, 0, 0, 0};
+      acc5_mac_fe(y, K.r, v0);
+      acc5_add_u64(y, K.b2);
+      return reduce_lo_acc5(y);
+    }
     return reduce_lo_acc5(x);                                  // mod p, then mod 2^64
   } else {
     const int tlast = (int)(B >> 2);
@@ -222,9 +264,16 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
     const uint32_t z0 = fetch(tlast), z1 = fetch(tlast + 1);
     uint32_t w = funnel(z0, z1, sh);
     w = (w & ((1u << (8 * r)) - 1)) | (1u << (8 * r));
-    if (tlast == 0) return w;
+    if (!V2 && tlast == 0) return w;
     mac32(A, (uint32_t)skeys[tlast], w);
     acc3_add_u64(A, K.b);
+    if constexpr (V2) {
+      const uint64_t v0 = reduce_acc3(A);
+      Acc3 y = {0, 0, 0};
+      acc3_mac_fe(y, (uint32_t)K.r, v0);
+      acc3_add_u64(y, K.b2);
+      return reduce_lo_acc3(y);
+    }
     return reduce_lo_acc3(A);
   }
 }
@@ -313,7 +362,7 @@ constexpr size_t kShortSmem = 256 /* keys */ + kByteRing + kSlack + 16 + (size_t
                               (size_t)kRing * sizeof(TileHdr) +
                               (size_t)(3 * kRing) * 8 + 128;
 
-template <int BITS>
+template <int BITS, bool V2 = false>
 __global__ void __launch_bounds__((kShortWarps + 1) * 32)
 k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets,
         uint64_t n, const OutSpec os, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
@@ -455,13 +504,13 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         // (lanes past n read the tile's first bytes: in bounds, result not stored)
         const uint32_t sofs = rpos + (valid ? (uint32_t)((uintptr_t)(bytes + o0) - (uintptr_t)ralo) : 0u);
         const uint32_t pa = ring_s + (sofs & ~3u);
-        lo = short_tree_lo<BITS>(K, skeys, B, 8 * (sofs & 3), tfm, [&](int kk) { return lds_u32(pa + 4 * kk); });
+        lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (sofs & 3), tfm, [&](int kk) { return lds_u32(pa + 4 * kk); });
       } else {
         // direct tile: read the string's aligned 32-bit words straight from global,
         // touching only words that overlap [start, end) (never past offsets[n]).
         const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
         const uintptr_t pa = sa & ~(uintptr_t)3;
-        lo = short_tree_lo<BITS>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, [&](int kk) {
+        lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, [&](int kk) {
           const uintptr_t a = pa + 4 * (uintptr_t)kk;
           return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
         });
@@ -593,9 +642,11 @@ template <int BITS> struct ChunkOut {
 
 // Processes chunks [cb, ce) (all inside one level-2 node).  Every lane returns
 // the same values.
-template <int BITS>
+// POLY (two-level variant, reading Q19): a2 is a table of 128 field elements
+// (lo, hi pairs) and chunk c is weighted by a2[(c + rot) mod 128].
+template <int BITS, bool POLY = false>
 PMP_DI ChunkOut<BITS> warp_chunks(const StrView &s, uint64_t cb, uint64_t ce, const LaneKeys<BITS> &lk,
-                                  uint64_t b1, const uint64_t *__restrict__ a2, int lane) {
+                                  uint64_t b1, const uint64_t *__restrict__ a2, int lane, uint32_t rot = 0) {
   using T = Tr<BITS>;
   using Acc = typename T::Acc;
   using Fe = typename T::Fe;
@@ -652,7 +703,15 @@ PMP_DI ChunkOut<BITS> warp_chunks(const StrView &s, uint64_t cb, uint64_t ce, co
       acc_add_word(x, b1);                      // Eq. (1): b_1 + sum a s
       const Fe v1 = acc_reduce(x);
       if (c == cb) res.v1_first = v1;
-      if (c < ce) acc_mac_fe(res.acc2, a2[c & 127], v1);
+      if constexpr (POLY) {
+        if (c < ce) {
+          Fe w;
+          fe_load(a2 + 2 * ((c + rot) & 127), w);
+          acc_mac_fe_full(res.acc2, w, v1);
+        }
+      } else {
+        if (c < ce) acc_mac_fe(res.acc2, a2[c & 127], v1);
+      }
     }
   }
   // sum the four groups' level-2 accumulators

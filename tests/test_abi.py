@@ -180,3 +180,19 @@ def test_keyfile_rejects_corrupt_files(L, bits):
         ok[o:o + w] = val.to_bytes(w, "little")
     pmp.Keys.load(bytes(ok))
     assert pmp.strerror(pmp.PMP_EKEYRANGE) == "key out of range"
+
+
+def test_two_level_variant_arguments(L):
+    """pmp_hash2_* validate like their tree counterparts and never fall back."""
+    k = pmp.Keys.generate(3, 64)
+    assert pmp.pmp_hash2_batch(0, 0, 0, 1, 0, 0) == pmp.PMP_EINVAL
+    assert pmp.pmp_hash2_batch(k.handle, 0, 0, 0, 0, 0) == 0
+    assert pmp.pmp_hash2_long(k.handle, 8, 10, 0, 0) == pmp.PMP_EINVAL              # out NULL
+    assert pmp.pmp_hash2_long_partial(k.handle, 1, 1000, 512, 5000, 1, 0) == pmp.PMP_EINVAL  # misaligned
+    assert pmp.pmp_hash2_long_partial(k.handle, 1, 1000, 1024, 5000, 1, 0) == pmp.PMP_EINVAL  # not whole blocks
+    assert pmp.pmp_hash2_long_combine(k.handle, 8, 0, 8, 0) == pmp.PMP_EINVAL
+    import torch
+
+    if not torch.cuda.is_available():
+        assert pmp.pmp_hash2_long(k.handle, 8, 10, 8, 0) == pmp.PMP_ENODEV
+        assert pmp.pmp_hash2_batch(k.handle, 8, 8, 1, 8, 0) == pmp.PMP_ENODEV
