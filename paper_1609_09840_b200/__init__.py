@@ -16,7 +16,9 @@ import os
 
 from . import _build
 
-LIB_PATH = _build.LIB
+# PMP_LIB_VARIANT: path of an in-tree tuning build (_build.build_variant), used by
+# the measurement tools to compare kernel parameters; defaults to libpmp.so.
+LIB_PATH = os.environ.get("PMP_LIB_VARIANT") or _build.LIB
 
 PMP_OK, PMP_EINVAL, PMP_ETOOLONG, PMP_ECUDA, PMP_ENOMEM, PMP_ENODEV = 0, -1, -2, -3, -4, -5
 PMP_EBADFILE, PMP_EVERSION, PMP_EKEYRANGE = -6, -7, -8

@@ -8,7 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpmp.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("pmp_api.cu", "pmp_kernels.cuh", "pmp_arith.cuh")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("pmp_api.cu", "pmp_kernels.cuh", "pmp_arith.cuh", "pmp_poly.cuh")] + [
     os.path.join(ROOT, "include", "pmp.h")
 ]
 
@@ -37,3 +37,14 @@ def build(force: bool = False, verbose: bool = False, nvcc: str = "nvcc") -> str
         subprocess.check_call(cmd)
         os.replace(tmp, LIB)
     return LIB
+
+
+def build_variant(name: str, defines: dict, nvcc: str = "nvcc") -> str:
+    """Tuning build: libpmp_<name>.so with -D overrides of the kernel
+    parameters (e.g. {"PMP_SHORT_RING_KB": 80}); selected at run time with
+    PMP_LIB_VARIANT.  The product build is always libpmp.so."""
+    out = os.path.join(PKG, f"libpmp_{name}.so")
+    cmd = [nvcc, *NVCC_FLAGS] + [f"-D{k}={v}" for k, v in defines.items()]
+    cmd += [os.path.join(CSRC, "pmp_api.cu"), "-o", out]
+    subprocess.check_call(cmd)
+    return out

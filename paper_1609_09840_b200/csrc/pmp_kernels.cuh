@@ -23,9 +23,23 @@ namespace pmp {
 
 constexpr uint32_t kShortMax = 127;      // bytes; k_short handles B <= kShortMax
 constexpr uint32_t kBigBytes = 1u << 16; // work-list class "big" (processed first)
-constexpr int kShortWarps = 16;          // consumer warps per k_short block (+1 producer)
+#ifndef PMP_SHORT_WARPS
+#define PMP_SHORT_WARPS 16
+#endif
+#ifndef PMP_SHORT_RING_KB
+#define PMP_SHORT_RING_KB 64
+#endif
+constexpr int kShortWarps = PMP_SHORT_WARPS;  // consumer warps per k_short block (+1 producer)
 constexpr int kWWarps = 4;               // warps per k_wstring / k_node block
 constexpr uint32_t FULL = 0xffffffffu;
+// k_short word-loop granularity (words between warp-uniform exit tests)
+#ifndef PMP_SHORT_G64
+#define PMP_SHORT_G64 4
+#endif
+#ifndef PMP_SHORT_G32
+#define PMP_SHORT_G32 8
+#endif
+constexpr int kShortG64 = PMP_SHORT_G64, kShortG32 = PMP_SHORT_G32;
 
 // level-1 keys 0..31 and b_1 passed by value: they live in the constant bank
 // and become immediate operands of the multiply-adds in k_short.
@@ -214,10 +228,10 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
     macc_zero(A);
     uint32_t y0 = fetch(0);
 #pragma unroll
-    for (int tb = 0; tb < 16; tb += 4) {
-      if (tb >= tfull_max) break;                              // warp-uniform, once per 4 words
+    for (int tb = 0; tb < 16; tb += kShortG64) {
+      if (tb >= tfull_max) break;                              // warp-uniform, once per kShortG64 words
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
+      for (int j = 0; j < kShortG64; j++) {
         const int t = tb + j;
         if (t >= 15) break;                                    // compile-time
         const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
@@ -248,10 +262,10 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
     Acc3 A = {0, 0, 0};
     uint32_t y0 = fetch(0);
 #pragma unroll
-    for (int tb = 0; tb < 32; tb += 8) {
-      if (tb >= tfull_max) break;                              // warp-uniform, once per 8 words
+    for (int tb = 0; tb < 32; tb += kShortG32) {
+      if (tb >= tfull_max) break;                              // warp-uniform, once per kShortG32 words
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
+      for (int j = 0; j < kShortG32; j++) {
         const int t = tb + j;
         if (t >= 31) break;
         const uint32_t y1 = fetch(t + 1);
@@ -328,6 +342,20 @@ PMP_DI void lds_hdr(uint32_t a, uint64_t &alo, uint32_t &pos, uint32_t &mode) { 
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(pos), "=r"(mode) : "r"(a));
   alo = ((uint64_t)y << 32) | x;
 }
+PMP_DI uint32_t atoms_add(uint32_t a, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
+  return r;
+}
+PMP_DI void sts_u32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+PMP_DI void sts_u16(uint32_t a, uint16_t v) { asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory"); }
+PMP_DI uint32_t lds_u16(uint32_t a) {
+  uint16_t r;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(a) : "memory");
+  return r;
+}
+// named barrier among the consumer warps only (id 0 is __syncthreads)
+PMP_DI void named_bar_sync(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 PMP_DI void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -349,7 +377,14 @@ PMP_DI void mbar_arrive(uint64_t *bar) {
 constexpr int kPasses = 1;                                     // strings per consumer lane per tile
 constexpr int kTile = 32 * kShortWarps * kPasses;              // 384
 constexpr int kRing = 8, kOffAhead = 4;
-constexpr uint32_t kByteRing = 64 * 1024;
+constexpr uint32_t kByteRing = PMP_SHORT_RING_KB * 1024;
+// Block-wide counting sort of each tile by word count before hashing
+// (PMP_SHORT_SORT=1): removes most of the zero-padding multiply-adds but costs
+// two named barriers per tile; measured 4-10% slower on configs[1]
+// (profiles/r01_summary.md), so it is off.
+#ifndef PMP_SHORT_SORT
+#define PMP_SHORT_SORT 0
+#endif
 constexpr uint32_t kSpanMaxTile = 32 * 1024;                   // larger spans go direct
 constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
 constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
@@ -360,7 +395,7 @@ struct TileHdr {
 };
 constexpr size_t kShortSmem = 256 /* keys */ + kByteRing + kSlack + 16 + (size_t)kRing * kOffBytes +
                               (size_t)kRing * sizeof(TileHdr) +
-                              (size_t)(3 * kRing) * 8 + 128;
+                              (size_t)(3 * kRing) * 8 + 256 /* sort histograms */ + 2 * kTile /* sort permutation */ + 128;
 
 template <int BITS, bool V2 = false>
 __global__ void __launch_bounds__((kShortWarps + 1) * 32)
@@ -375,7 +410,10 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   uint64_t *bar_off = reinterpret_cast<uint64_t *>(hdr + kRing);  // offsets landed (producer)
   uint64_t *bar_done = bar_off + kRing;                            // tile consumed (producer)
   uint64_t *bar_full = bar_done + kRing;                           // tile ready (consumers)
+  uint32_t *s_hist = reinterpret_cast<uint32_t *>(bar_full + kRing);  // 2 x 32 class counters
+  uint16_t *s_perm = reinterpret_cast<uint16_t *>(s_hist + 64);      // kTile sorted slots
   if (threadIdx.x < 32) skeys[threadIdx.x] = K.a[threadIdx.x];
+  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     for (int q = 0; q < kRing; q++) {
       mbar_init(&bar_off[q], 1);
@@ -466,20 +504,25 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   const uint32_t offs_s = smem_u32(offs) + 8u * (32u * wib + lane);
   const uint32_t hdr_s = smem_u32(hdr), full_s = smem_u32(bar_full), done_s = smem_u32(bar_done);
   const uint64_t tstride = (uint64_t)gridDim.x * kTile;
-  uint64_t i = (uint64_t)blockIdx.x * kTile + 32 * wib + lane;
-  for (uint32_t k = 0; k < my_tiles; k++, i += tstride) {
+  const uint32_t ct = 32u * wib + lane;                 // consumer thread = string slot in the tile
+#if PMP_SHORT_SORT
+  const uint32_t offs0_s = smem_u32(offs), hist_s = smem_u32(s_hist), perm_s = smem_u32(s_perm);
+#endif
+  uint64_t ibase = (uint64_t)blockIdx.x * kTile;
+  for (uint32_t k = 0; k < my_tiles; k++, ibase += tstride) {
     const uint32_t q = k & (kRing - 1);
+    uint64_t i = ibase + ct;
     mbar_wait_s(full_s + 8 * q, (k / kRing) & 1);
     uint64_t ralo;
     uint32_t rpos, mode;
     lds_hdr(hdr_s + 16 * q, ralo, rpos, mode);
-    const bool valid = i < n;
+    bool valid = i < n;
     uint64_t o0, o1;
     lds_u64x2(offs_s + q * kOffBytes, o0, o1);      // offsets[i], offsets[i+1] (slot-local)
     const uint64_t Bl = valid ? o1 - o0 : 0;
-    const bool is_short = Bl <= kShortMax;           // invalid lanes: an empty string, not stored
+    bool is_short = Bl <= kShortMax;                 // invalid lanes: an empty string, not stored
     const bool is_long = !is_short;
-    const uint32_t B = (uint32_t)Bl;
+    uint32_t B = (uint32_t)Bl;
     const unsigned longmask = __ballot_sync(FULL, is_long);
     if (longmask) {
       // warp-aggregated append: big strings from the back, others from the front
@@ -496,6 +539,39 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
       if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
       if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
     }
+#if PMP_SHORT_SORT
+    // ---- counting sort of the tile's strings by word count (block-wide, two
+    // named barriers): warp w then hashes sorted strings 32w..32w+31, whose
+    // word counts differ by at most one class, so the word loop below runs
+    // to (almost) every lane's own length instead of the longest string of
+    // 32 random ones.  Long / past-n strings sort last and are skipped.
+    {
+      const uint32_t cls = is_short ? min(B / (uint32_t)(BITS / 8), 30u) : 31u;
+      const uint32_t hb = hist_s + 128u * (k & 1);
+      const uint32_t rank = atoms_add(hb + 4 * cls, 1u);
+      named_bar_sync(1, kShortWarps * 32);
+      const uint32_t h = lds_u32(hb + 4 * lane);
+      uint32_t incl = h;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const uint32_t start = __shfl_sync(FULL, incl - h, (int)cls);
+      sts_u16(perm_s + 2 * (start + rank), (uint16_t)ct);
+      named_bar_sync(1, kShortWarps * 32);
+      if (ct < 32) sts_u32(hb + 4 * ct, 0u);
+      const uint32_t j = lds_u16(perm_s + 2 * ct);
+      uint64_t p0, p1;
+      lds_u64x2(offs0_s + q * kOffBytes + 8 * j, p0, p1);
+      i = ibase + j;
+      valid = i < n;
+      o0 = p0;
+      const uint64_t Bj = valid ? p1 - p0 : 0;
+      is_short = Bj <= kShortMax;
+      B = (uint32_t)Bj;
+    }
+#endif
     // warp max of the number of full words (the marker word is handled apart)
     const int tfm = (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
     if (is_short) {
