@@ -410,10 +410,12 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   uint64_t *bar_off = reinterpret_cast<uint64_t *>(hdr + kRing);  // offsets landed (producer)
   uint64_t *bar_done = bar_off + kRing;                            // tile consumed (producer)
   uint64_t *bar_full = bar_done + kRing;                           // tile ready (consumers)
+  if (threadIdx.x < 32) skeys[threadIdx.x] = K.a[threadIdx.x];
+#if PMP_SHORT_SORT
   uint32_t *s_hist = reinterpret_cast<uint32_t *>(bar_full + kRing);  // 2 x 32 class counters
   uint16_t *s_perm = reinterpret_cast<uint16_t *>(s_hist + 64);      // kTile sorted slots
-  if (threadIdx.x < 32) skeys[threadIdx.x] = K.a[threadIdx.x];
   if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
+#endif
   if (threadIdx.x == 0) {
     for (int q = 0; q < kRing; q++) {
       mbar_init(&bar_off[q], 1);
