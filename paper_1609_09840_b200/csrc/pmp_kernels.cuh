@@ -106,6 +106,8 @@ PMP_DI Acc5 acc_shfl_xor(const Acc5 &x, int m) { return acc5_shfl_xor(x, m); }
 PMP_DI Acc3 acc_shfl_xor(const Acc3 &x, int m) { return acc3_shfl_xor(x, m); }
 PMP_DI Fe64 acc_reduce(const Acc5 &x) { return reduce_acc5(x); }
 PMP_DI uint64_t acc_reduce(const Acc3 &x) { return reduce_acc3(x); }
+PMP_DI uint64_t acc_reduce_lo(const Acc5 &x) { return reduce_lo_acc5(x); }  // V mod 2^n only
+PMP_DI uint64_t acc_reduce_lo(const Acc3 &x) { return reduce_lo_acc3(x); }
 PMP_DI uint64_t fe_lo(const Fe64 &v) { return v.lo; }
 PMP_DI uint64_t fe_lo(uint64_t v) { return (uint32_t)v; }
 PMP_DI void fe_store(uint64_t *dst, const Fe64 &v) { dst[0] = v.lo; dst[1] = v.hi; }
@@ -825,69 +827,57 @@ PMP_HDI Geom make_geom(uint64_t Twords) {
 
 // ============================================================= k_wstring
 // Warp per string from the work list (big strings first).  Each warp streams
-// its strings through a private shared-memory ring of 4 KiB tiles: lane 0
-// issues TMA bulk copies up to kWStages-1 tiles ahead, across string
-// boundaries (it prefetches the next work item while the current string is
-// being issued), and the warp hashes tile t while tiles t+1.. are in flight.
+// its strings through a private shared-memory ring of 4 KiB tiles fed by TMA
+// bulk copies (one elected lane issues them), up to kWStages tiles ahead and
+// across string boundaries, and hashes tile t while tiles t+1.. are in flight.
+// The issue side is warp-uniform: every lane holds the same cursor (item,
+// tile) in registers, so feeding a tile costs a few dozen instructions and no
+// divergent single-lane code.  Work items: big strings (>= kBigBytes, listed
+// from the back of the work list) are claimed dynamically through a small
+// non-blocking claim pipeline (atomic -> work-list entry -> offsets, one
+// stage per issued tile); mid strings are strided statically over the warps,
+// their offsets fetched 32 at a time, one per lane, one batch ahead.
 // A tile is 4 level-1 blocks (PM+64) / 8 (PM+32) of one string; its copy
 // starts at the 16-byte aligned address at or below the string's byte 4096 t
 // and carries 16 bytes of overlap, so a misaligned string is realigned from
-// shared memory (5 x LDS.32 + funnel shifts per 16 bytes) without shuffles.
+// shared memory (3 loads + funnel shifts per 16 bytes) without shuffles.
 // Level 2 is accumulated per lane group and closed every 128 blocks; levels
 // >= 3 are streamed by lane 0 (bounded memory).
 constexpr int kWTile = 4096;
-constexpr int kWStages = 2;
+#ifndef PMP_W_STAGES
+#define PMP_W_STAGES 2
+#endif
+constexpr int kWStages = PMP_W_STAGES;
 constexpr int kWStageBytes = kWTile + 32;      // + 16 B overlap + 16 B read slack
 constexpr int kWBlockWarps = 4;
 struct WStack {      // lane 0's streaming state for levels 3..8
   uint64_t T[kL + 1];
   uint64_t pushed[kL - 2];
   uint32_t up[kL - 2][5];
-  // the warp's current 32 work items, geometry precomputed in parallel
-  uint64_t qsa[32];                    // address of the string's first byte
-  uint64_t qB[32];                     // length
-  uint32_t qi[32];                     // string index
-  uint32_t qnt[32];                    // tiles | fold flag << 31
-  uint64_t bsa, bB;                    // the claimed big string (lane 0)
-  uint32_t bi, bnt;
 };
-struct WProd {      // lane 0's producer state (kept in shared memory, not registers)
-  uint64_t p_sa, p_B;                  // string being issued
-  uint32_t p_i, p_nt;                  // index, tiles | fold << 31
-  uint32_t p_tile, p_item, p_have, need_batch;
-  uint32_t bg_have, issued, pq, pad;
-};
-struct WHdr {
-  uint64_t i;        // string index
+struct WHdr {        // one per stage, written by the issuing lane
+  uint64_t sa;       // address of the string's byte 0
   uint64_t B;        // string length
+  uint32_t i;        // string index
   uint32_t tile;     // tile index within the string
-  uint32_t ntiles;
-  uint32_t delta;    // string start & 15
-  uint32_t pad;
+  uint32_t nt;       // tiles | fold flag << 31
+  uint32_t nb;       // bytes copied (0: the tile holds only a marker-only block)
 };
 constexpr size_t kWSmemPerWarp =
-    ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + sizeof(WProd) + 15) & ~(size_t)15;
+    ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + 15) & ~(size_t)15;
 // block region: a_{2,0..127}, b_1..8, and the key-only values a_{2,r} * (b_1 + a_{1,0}) mod p
 // (lo words, then hi bits) of a marker-only level-1 block at position r
 constexpr size_t kWBlockRegion = 1024 + 64 + 1024 + 512 + 1024 /* a_{1,0..127} */;
 constexpr size_t kWSmem = kWBlockRegion + kWBlockWarps * kWSmemPerWarp;
 
+#ifndef PMP_W_EARLY
+#define PMP_W_EARLY 0
+#endif
+#ifndef PMP_W_MINB
+#define PMP_W_MINB 5
+#endif
 template <int BITS>
-PMP_DI uint4 tile_unit(uint32_t stage_s, uint32_t delta, uint32_t off) {
-  if (delta == 0) {
-    uint4 u;
-    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
-                 : "r"(stage_s + off));
-    return u;
-  }
-  const uint32_t a = stage_s + ((delta + off) & ~3u), sh = 8 * (delta & 3);
-  const uint32_t y0 = lds_u32(a), y1 = lds_u32(a + 4), y2 = lds_u32(a + 8), y3 = lds_u32(a + 12),
-                 y4 = lds_u32(a + 16);
-  return make_uint4(funnel(y0, y1, sh), funnel(y1, y2, sh), funnel(y2, y3, sh), funnel(y3, y4, sh));
-}
-
-template <int BITS>
-__global__ void __launch_bounds__(kWBlockWarps * 32, 5)
+__global__ void __launch_bounds__(kWBlockWarps * 32, PMP_W_MINB)
 k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
           const uint64_t *__restrict__ offsets, uint64_t n, const OutSpec os,
           const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
@@ -908,12 +898,10 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   WHdr *hdr = reinterpret_cast<WHdr *>(wbase + (size_t)kWStages * kWStageBytes);
   uint64_t *bar = reinterpret_cast<uint64_t *>(hdr + kWStages);
   WStack *stk = reinterpret_cast<WStack *>(bar + kWStages);
-  WProd *pr = reinterpret_cast<WProd *>(stk + 1);
   const uint64_t *bk = keys;           // b_1..b_8
   const uint64_t *ak = keys + kL;      // a_{j,i} at ak[(j-1)*128 + i]
   const uint32_t nmid = wcount[0], nbig = wcount[1];
-  const uint32_t total = nmid + nbig;
-  if (total == 0) return;
+  if (nmid + nbig == 0) return;
   for (int k = threadIdx.x; k < (int)kM; k += blockDim.x) {
     s_a2[k] = ak[kM + k];
     // a marker-only level-1 block (sigma = 1, 0, ..., 0) has v_1 = b_1 + a_{1,0} mod p
@@ -928,153 +916,142 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     fe_store(w2, m);
     s_mklo[k] = w2[0];
     s_mkhi[k] = (uint32_t)w2[1];
-  }
-  if (threadIdx.x < kL) s_b[threadIdx.x] = bk[threadIdx.x];
-  for (int k = threadIdx.x; k < (int)kM; k += blockDim.x) {
     if constexpr (BITS == 64) s_a1[k] = ak[k];
     else reinterpret_cast<uint32_t *>(s_a1)[k] = (uint32_t)ak[k];
   }
-  __syncthreads();
-  const uint64_t b1 = s_b[0], b2 = s_b[1], a10 = ak[0];
-  const uint32_t a1_s = smem_u32(s_a1);
+  if (threadIdx.x < kL) s_b[threadIdx.x] = bk[threadIdx.x];
   if (lane == 0) {
     for (int q = 0; q < kWStages; q++) mbar_init(&bar[q], 1);
     mbar_fence_init();
   }
-  __syncwarp();
+  __syncthreads();
+  const uint64_t b1 = s_b[0], b2 = s_b[1], a10 = ak[0];
+  const uint32_t a1_s = smem_u32(s_a1);
   const uint32_t stg_s = smem_u32(stg);
 
-  // ---- work items.  Big strings (>= kBigBytes, listed first) are claimed
-  // dynamically, one at a time, by lane 0 with a one-item prefetch (a big
-  // string spans >= 16 tiles, which hides the claim latency) so that the
-  // largest strings spread evenly over the warps.  Mid strings are strided
-  // statically (item k of this warp = gw + k * nw); their metadata is fetched
-  // 32 items at a time, one per lane, into registers one batch ahead and
-  // parked in a shared-memory queue that lane 0 (the producer) reads.
-  const uint32_t gw = blockIdx.x * kWBlockWarps + wib, nw = gridDim.x * kWBlockWarps;
-  uint64_t r_i = 0, r_o0 = 0, r_o1 = 0;      // lane's item of the next batch (in flight)
-  auto fetch_batch = [&](uint32_t kbase) {   // all lanes: mid items kbase + lane
-    const uint32_t item = gw + (kbase + lane) * nw;
-    if (item < nmid) {
-      r_i = wlist[item];
-      r_o0 = offsets[r_i];
-      r_o1 = offsets[r_i + 1];
-    }
-  };
   // tile count of a string and whether its last tile is folded: a trailing
   // tile holding only a marker-only block (no data bytes) is folded into the
   // previous tile unless that block opens a level-2 node
   auto tiles_of = [&](uint64_t sa, uint64_t B) -> uint32_t {
-    const uintptr_t A = sa & ~(uint64_t)15;
+    const uint64_t A = sa & ~(uint64_t)15;
     const uint64_t nbytes = ((sa + B + 15) & ~(uint64_t)15) - A;
     const uint64_t T1 = (B / W + 1 + 127) / 128;           // level-1 blocks
     uint32_t nt = (uint32_t)((T1 + CPI - 1) / CPI);
     const bool fold = nt > 1 && (uint64_t)(nt - 1) * kWTile >= nbytes && ((T1 - 1) & 127) != 0;
     return fold ? (nt - 1) | 0x80000000u : nt;
   };
-  uint32_t qbase = 0;                        // item number of queue entry 0
-  auto park_batch = [&]() {                  // all lanes: registers -> queue, fetch the next batch
-    const uint64_t sa = (uint64_t)(uintptr_t)(bytes + r_o0), B = r_o1 - r_o0;
-    stk->qsa[lane] = sa;
-    stk->qB[lane] = B;
-    stk->qi[lane] = (uint32_t)r_i;
-    stk->qnt[lane] = tiles_of(sa, B);
-    __syncwarp();
-    fetch_batch(qbase + 32);
+
+  // ---- work-item source (warp-uniform state) ----
+  const uint32_t gw = blockIdx.x * kWBlockWarps + wib, nw = gridDim.x * kWBlockWarps;
+  // big strings: claim pipeline.  cl = 0 idle/exhausted, 1 atomic issued (lane 0),
+  // 2 work-list entry loading, 3 offsets loading; each step consumes the
+  // previous step's load, so it only stalls if that load is still in flight.
+  uint32_t cl = 0, cl_item = 0, cl_bi = 0;
+  uint64_t cl_o0 = 0, cl_o1 = 0;
+  bool big_open = nbig > 0;
+  auto claim_step = [&]() {
+    if (cl == 1) {
+      cl_item = __shfl_sync(FULL, cl_item, 0);
+      if (cl_item < nbig) {
+        cl_bi = wlist[n - 1 - cl_item];
+        cl = 2;
+      } else {
+        cl = 0;
+        big_open = false;
+      }
+    } else if (cl == 2) {
+      cl_o0 = offsets[cl_bi];
+      cl_o1 = offsets[cl_bi + 1];
+      cl = 3;
+    }
+  };
+  auto claim_start = [&]() {
+    if (lane == 0) cl_item = atomicAdd(&wcount[2], 1u);
+    cl = 1;
+  };
+  if (big_open) claim_start();
+  // mid strings: item k of this warp = gw + k * nw; lane e holds item 32 b + e of
+  // the current batch b (cur) and of the next one (nxt, loads in flight)
+  uint32_t mk = 0;                                   // mid items taken
+  uint32_t cur_i = 0, nxt_i = 0;
+  uint64_t cur_o0 = 0, cur_o1 = 0, nxt_o0 = 0, nxt_o1 = 0;
+  auto fetch_batch = [&](uint32_t kbase) {           // item kbase + lane -> nxt
+    const uint32_t item = gw + (kbase + lane) * nw;
+    if (item < nmid) {
+      nxt_i = wlist[item];
+      nxt_o0 = offsets[nxt_i];
+      nxt_o1 = offsets[nxt_i + 1];
+    }
   };
   fetch_batch(0);
-  park_batch();
-  // big-string claim (lane 0): the next big item, prefetched
-  auto claim_big = [&]() {
-    pr->bg_have = 0;
-    if (nbig == 0) return;
-    const uint32_t item = atomicAdd(&wcount[2], 1u);
-    if (item < nbig) {
-      const uint64_t bi = wlist[n - 1 - item];
-      const uint64_t o0 = offsets[bi], o1 = offsets[bi + 1];
-      stk->bsa = (uint64_t)(uintptr_t)(bytes + o0);
-      stk->bB = o1 - o0;
-      stk->bi = (uint32_t)bi;
-      pr->bg_have = 1;
+  // next item into (sa, B, i); false when the warp's work is exhausted
+  auto next_item = [&](uint64_t &sa, uint64_t &B, uint32_t &i) -> bool {
+    while (big_open) {
+      if (cl == 3) {
+        sa = (uint64_t)(uintptr_t)(bytes + cl_o0);
+        B = cl_o1 - cl_o0;
+        i = cl_bi;
+        claim_start();
+        return true;
+      }
+      claim_step();                                   // (blocks on the pending load)
     }
+    const uint32_t item = gw + mk * nw;
+    if (item >= nmid) return false;
+    const int e = (int)(mk & 31);
+    if (e == 0) {                                     // rotate: next batch becomes current
+      cur_i = nxt_i;
+      cur_o0 = nxt_o0;
+      cur_o1 = nxt_o1;
+      fetch_batch(mk + 32);
+    }
+    const uint64_t o0 = __shfl_sync(FULL, cur_o0, e), o1 = __shfl_sync(FULL, cur_o1, e);
+    i = __shfl_sync(FULL, cur_i, e);
+    sa = (uint64_t)(uintptr_t)(bytes + o0);
+    B = o1 - o0;
+    mk++;
+    return true;
   };
-  if (lane == 0) {
-    pr->p_have = 0;
-    pr->p_item = 0;
-    pr->need_batch = 0;
-    pr->issued = 0;
-    pr->pq = 0;
-    claim_big();
-  }
-  uint32_t issued = 0, consumed = 0;
-  auto produce = [&]() {  // lane 0: fill free ring slots (state in shared memory)
-    uint32_t iss = pr->issued, pq = pr->pq;
-    while (iss - consumed < (uint32_t)kWStages) {
-      uint32_t tile = pr->p_tile;
-      if (!pr->p_have || tile == (pr->p_nt & 0x7fffffffu)) {
-        if (pr->bg_have) {
-          pr->p_sa = stk->bsa;
-          pr->p_B = stk->bB;
-          pr->p_i = stk->bi;
-          pr->p_nt = tiles_of(stk->bsa, stk->bB);
-          claim_big();
-        } else {
-          const uint32_t pi = pr->p_item;
-          const uint32_t item = gw + pi * nw;
-          if (item >= nmid) break;
-          if (pi - qbase >= 32) {            // queue exhausted: the warp must park the next batch
-            pr->need_batch = 1;
-            break;
-          }
-          const int e = (int)(pi - qbase);
-          pr->p_sa = stk->qsa[e];
-          pr->p_B = stk->qB[e];
-          pr->p_i = stk->qi[e];
-          pr->p_nt = stk->qnt[e];
-          pr->p_item = pi + 1;
+
+  // ---- issue side (warp-uniform cursor) ----
+  uint64_t p_sa = 0, p_B = 0;
+  uint32_t p_i = 0, p_nt = 0, p_tile = 0;
+  bool p_have = false, p_done = false;
+  uint32_t issued = 0, consumed = 0, pq = 0;
+  auto produce = [&]() {
+    while (!p_done && issued - consumed < (uint32_t)kWStages) {
+      if (!p_have || p_tile == (p_nt & 0x7fffffffu)) {
+        if (!next_item(p_sa, p_B, p_i)) {
+          p_done = true;
+          break;
         }
-        pr->p_have = 1;
-        tile = 0;
+        p_nt = tiles_of(p_sa, p_B);
+        p_tile = 0;
+        p_have = true;
       }
-      const uint64_t sa = pr->p_sa, B = pr->p_B;
-      const uint32_t nt = pr->p_nt, ntiles = nt & 0x7fffffffu;
-      const uint64_t A = sa & ~(uint64_t)15;
-      const uint64_t nbytes = ((sa + B + 15) & ~(uint64_t)15) - A;
-      const int q = (int)pq;
-      pq = pq + 1 == (uint32_t)kWStages ? 0u : pq + 1;
-      const uint64_t off = (uint64_t)tile * kWTile;
+      const uint64_t A = p_sa & ~(uint64_t)15;
+      const uint64_t nbytes = ((p_sa + p_B + 15) & ~(uint64_t)15) - A;
+      const uint64_t off = (uint64_t)p_tile * kWTile;
       const uint32_t nb = off < nbytes ? (uint32_t)min((uint64_t)(kWTile + 16), nbytes - off) : 0u;
-      hdr[q].i = pr->p_i;
-      hdr[q].B = B;
-      hdr[q].tile = tile;
-      hdr[q].ntiles = ntiles;
-      hdr[q].delta = (uint32_t)(sa & 15) | (((nt >> 31) && tile + 1 == ntiles) ? 0x100u : 0u);
-      hdr[q].pad = nb;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the slot
-      mbar_arrive_tx(&bar[q], nb);
-      if (nb) bulk_g2s(stg + (size_t)q * kWStageBytes, reinterpret_cast<const void *>(A + off), nb, &bar[q]);
-      pr->p_tile = tile + 1;
-      iss++;
-    }
-    pr->issued = iss;
-    pr->pq = pq;
-  };
-  auto refill = [&]() {   // all lanes
-    for (;;) {
-      uint32_t nb = 0;
       if (lane == 0) {
-        produce();
-        issued = pr->issued;
-        nb = pr->need_batch;
+        WHdr &h = hdr[pq];
+        h.sa = p_sa;
+        h.B = p_B;
+        h.i = p_i;
+        h.tile = p_tile;
+        h.nt = p_nt;
+        h.nb = nb;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the slot
+        mbar_arrive_tx(&bar[pq], nb);
+        if (nb) bulk_g2s(stg + (size_t)pq * kWStageBytes, reinterpret_cast<const void *>(A + off), nb, &bar[pq]);
       }
-      issued = __shfl_sync(FULL, issued, 0);
-      if (__shfl_sync(FULL, nb, 0) == 0) break;
-      if (lane == 0) pr->need_batch = 0;
-      qbase += 32;
-      park_batch();
+      pq = pq + 1 == (uint32_t)kWStages ? 0u : pq + 1;
+      p_tile++;
+      issued++;
+      if (cl == 1 || cl == 2) claim_step();          // advance the big claim one step per tile
     }
   };
-  refill();
+  produce();
 
   // ---- consumer state (whole warp): the string being hashed
   uint64_t tlast = 0, T1 = 0;
@@ -1091,18 +1068,19 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       cq = 0;
       cph ^= 1;
     }
-    const uint64_t si = hdr[q].i;
-    const uint32_t t = hdr[q].tile, ntiles = hdr[q].ntiles, delta = hdr[q].delta & 15;
-    const bool fold = (hdr[q].delta & 0x100u) != 0; // + the string's marker-only last block
-    const bool nodata = hdr[q].pad == 0;            // only the marker word (= 1) at word 128*c0
-    if (t == 0) {                                   // a new string starts
-      const uint64_t B = hdr[q].B;
+    const WHdr &h = hdr[q];
+    const uint32_t si = h.i, t = h.tile, ntiles = h.nt & 0x7fffffffu;
+    const uint32_t delta = (uint32_t)h.sa & 15u;
+    const bool fold = (h.nt >> 31) && t + 1 == ntiles; // + the string's marker-only last block
+    const bool nodata = h.nb == 0;                   // only the marker word (= 1) at word 128*c0
+    if (t == 0) {                                    // a new string starts
+      const uint64_t B = h.B;
       tlast = B / W;
       rbytes = (uint32_t)(B % W);
       T1 = (tlast + 1 + 127) / 128;
-      leff = levels_of(tlast + 1);
+      leff = tlast == 0 ? 0 : T1 == 1 ? 1 : T1 <= 128 ? 2 : levels_of(tlast + 1);
       acc_zero(acc2);
-      if (leff >= 3 && lane == 0) {                 // streaming state for levels >= 3
+      if (leff >= 3 && lane == 0) {                  // streaming state for levels >= 3
         const Geom gm = make_geom(tlast + 1);
         for (int j = 0; j <= (int)kL; j++) stk->T[j] = gm.T[j];
         for (int j = 0; j < (int)kL - 2; j++) {
@@ -1151,6 +1129,12 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
         for (int j = 0; j < 8; j++) fixup_unit<BITS>(U[j], tw0 + (uint64_t)(16 * (r + 8 * j)) / W, tlast, rbytes);
       }
     }
+#if PMP_W_EARLY
+    // the tile is in registers: refill its slot before the multiply-adds
+    __syncwarp();
+    consumed++;
+    produce();
+#endif
     // ---- level-1 multiply-accumulate (the hot loop) ----
     Acc part[CPG];
     if (nodata) {
@@ -1191,10 +1175,12 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       part[0] = A[0];
       part[CPG - 1] = A[1];
     }
+#if !PMP_W_EARLY
     __syncwarp();
-    // the slot is free: let lane 0 refill the ring before the reductions
+    // the slot is free: refill the ring before the reductions
     consumed++;
-    refill();
+    produce();
+#endif
     // ---- combine the 8 lanes of each group, fold into level 2 ----
 #pragma unroll
     for (int cs = 0; cs < CPG; cs++) {
@@ -1231,10 +1217,12 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       }
       acc_zero(acc2);
       acc_add_word(x, b2);                          // b_2
-      Fe v = acc_reduce(x);                         // v_{2,q}
       if (leff == 2) {
-        root = v;
-      } else if (lane == 0) {
+        if (lane == 0) emit<BITS>(os, si, acc_reduce_lo(x));  // V mod 2^n
+        continue;
+      }
+      Fe v = acc_reduce(x);                         // v_{2,q}
+      if (lane == 0) {
         // push v into level 3, carrying completed nodes upward
         for (int j = 3; j <= leff; j++) {
           const int li = j - 3;
@@ -1254,7 +1242,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
         }
       }
     }
-    if (t + 1 == ntiles) {
+    if (t + 1 == ntiles && leff != 2) {
       if (leff == 1) root = fe_shfl(root, 0);
       if (lane == 0) emit<BITS>(os, si, fe_lo(root));
     }
