@@ -693,8 +693,18 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     cudaFuncSetAttribute(k_wstring<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
     cudaFuncSetAttribute(k_wstring<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
   });
-  const uint64_t wper_sm = (228u * 1024u) / (kWSmem + 1024u);
-  const unsigned wgrid = (unsigned)(sms * (wper_sm ? wper_sm : 1));  // persistent, work list drained by atomics
+  // persistent grid: exactly the resident blocks (registers and shared memory),
+  // since mid strings are strided statically over the warps
+  static int wper_sm[2] = {0, 0};
+  int &wps = wper_sm[k->bits == 64];
+  if (wps == 0) {
+    if (k->bits == 64)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wps, k_wstring<64>, kWBlockWarps * 32, kWSmem);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wps, k_wstring<32>, kWBlockWarps * 32, kWSmem);
+    if (wps < 1) wps = 1;
+  }
+  const unsigned wgrid = (unsigned)(sms * wps);
   if (k->bits == 64)
     rc = launch("k_wstring", st, [&] { k_wstring<64><<<wgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
   else
