@@ -356,7 +356,7 @@ def main():
                     fn = pmp.pmp_hash2_batch if v2 else pmp.pmp_hash_batch
                     pmp._check(fn(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
                                   outs[b].data_ptr(), sp), "pmp_hash_batch")
-        dominant = "k_short" if wl.hi <= 127 else ("k_poly_wstring" if v2 else "k_wstring")
+        dominant = "k_short" if wl.hi <= 127 else "k_wstring"
         # algorithmic bytes per dominant launch: payload + offsets + digests (avg over widths)
         alg_bytes_per_launch = total_bytes + 8 * (n + 1) + n * sum(b // 8 for b in wl.bits) / len(wl.bits)
     torch.cuda.synchronize()

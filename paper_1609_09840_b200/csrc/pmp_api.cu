@@ -678,10 +678,24 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     else
       rc = launch("k_short", st, [&] { k_short<32, true><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
     if (rc) return rc;
-    const unsigned pgrid = (unsigned)(sms * 16);
+    static std::once_flag pattr_once;
+    std::call_once(pattr_once, [] {
+      cudaFuncSetAttribute(k_wstring<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+      cudaFuncSetAttribute(k_wstring<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+    });
+    static int pper_sm[2] = {0, 0};
+    int &pps = pper_sm[k->bits == 64];
+    if (pps == 0) {
+      if (k->bits == 64)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pps, k_wstring<64, true>, kWBlockWarps * 32, kWSmem);
+      else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pps, k_wstring<32, true>, kWBlockWarps * 32, kWSmem);
+      if (pps < 1) pps = 1;
+    }
+    const unsigned pgrid = (unsigned)(sms * pps);
     if (k->bits == 64)
-      return launch("k_poly_wstring", st, [&] { k_poly_wstring<64><<<pgrid, kWWarps * 32, 0, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
-    return launch("k_poly_wstring", st, [&] { k_poly_wstring<32><<<pgrid, kWWarps * 32, 0, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
+      return launch("k_wstring", st, [&] { k_wstring<64, true><<<pgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
+    return launch("k_wstring", st, [&] { k_wstring<32, true><<<pgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
   }
   if (k->bits == 64)
     rc = launch("k_short", st, [&] { k_short<64><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });

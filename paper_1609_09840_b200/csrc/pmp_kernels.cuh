@@ -843,6 +843,33 @@ PMP_HDI Geom make_geom(uint64_t Twords) {
 // shared memory (3 loads + funnel shifts per 16 bytes) without shuffles.
 // Level 2 is accumulated per lane group and closed every 128 blocks; levels
 // >= 3 are streamed by lane 0 (bounded memory).
+// POLY: the two-level variant (reading Q19): the same
+// level-1 chunk values, combined by V = b_2 + sum_c v_c r^(C-c) instead of the
+// tree.  With d = (-C) mod 128 virtual leading zero chunks, chunk c sits at
+// position i = (c + d) mod 128 of virtual node q = (c + d) / 128 and
+// r^(C-c) = W[i] R^(Q-1-q) (pmp_poly.cuh), so the pipeline is the tree's with
+// a_{2,i} replaced by W[i], node boundaries shifted by d, and each closed node
+// weighted by a power of R = r^128 and summed.
+constexpr uint32_t kPolyW = kL + kL * kM;    // blob word offset of W[0..128) = r^(128-i) (lo, hi pairs)
+constexpr uint32_t kPolyLadder = 48;         // R^(2^k), k < 48 (Q < 2^42 for T < 2^56)
+constexpr uint32_t kPolyRP = kPolyW + 2 * kM;
+constexpr uint32_t kBlobWords = kPolyRP + 2 * kPolyLadder;
+
+// R^e from the square ladder RP[k] = R^(2^k) (same value in every lane)
+template <int BITS>
+PMP_DI typename Tr<BITS>::Fe poly_pow_R(const uint64_t *__restrict__ keys, uint64_t e) {
+  using Fe = typename Tr<BITS>::Fe;
+  Fe w = fe_from_word(1, (Fe *)nullptr);
+  for (uint32_t k = 0; e; k++, e >>= 1) {
+    if (e & 1) {
+      Fe f;
+      fe_load(keys + kPolyRP + 2 * k, f);
+      w = fe_mul(w, f);
+    }
+  }
+  return w;
+}
+
 constexpr int kWTile = 4096;
 #ifndef PMP_W_STAGES
 #define PMP_W_STAGES 2
@@ -865,8 +892,10 @@ struct WHdr {        // one per stage, written by the issuing lane
 };
 constexpr size_t kWSmemPerWarp =
     ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + 15) & ~(size_t)15;
-// block region: a_{2,0..127}, b_1..8, and the key-only values a_{2,r} * (b_1 + a_{1,0}) mod p
-// (lo words, then hi bits) of a marker-only level-1 block at position r
+// block region: a_{2,0..127} (POLY: W[0..127] lo words), b_1..8, the key-only
+// values a_{2,r} * (b_1 + a_{1,0}) mod p (lo words, then hi bits) of a
+// marker-only level-1 block at position r (POLY: lo words unused, hi words =
+// W hi bits), a_{1,0..127}
 constexpr size_t kWBlockRegion = 1024 + 64 + 1024 + 512 + 1024 /* a_{1,0..127} */;
 constexpr size_t kWSmem = kWBlockRegion + kWBlockWarps * kWSmemPerWarp;
 
@@ -876,7 +905,7 @@ constexpr size_t kWSmem = kWBlockRegion + kWBlockWarps * kWSmemPerWarp;
 #ifndef PMP_W_MINB
 #define PMP_W_MINB 5
 #endif
-template <int BITS>
+template <int BITS, bool POLY = false>
 __global__ void __launch_bounds__(kWBlockWarps * 32, PMP_W_MINB)
 k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
           const uint64_t *__restrict__ offsets, uint64_t n, const OutSpec os,
@@ -903,6 +932,13 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   const uint32_t nmid = wcount[0], nbig = wcount[1];
   if (nmid + nbig == 0) return;
   for (int k = threadIdx.x; k < (int)kM; k += blockDim.x) {
+    if constexpr (POLY) {
+      s_a2[k] = keys[kPolyW + 2 * k];
+      s_mkhi[k] = (uint32_t)keys[kPolyW + 2 * k + 1];
+      if constexpr (BITS == 64) s_a1[k] = ak[k];
+      else reinterpret_cast<uint32_t *>(s_a1)[k] = (uint32_t)ak[k];
+      continue;
+    }
     s_a2[k] = ak[kM + k];
     // a marker-only level-1 block (sigma = 1, 0, ..., 0) has v_1 = b_1 + a_{1,0} mod p
     Acc x, y;
@@ -926,6 +962,14 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   }
   __syncthreads();
   const uint64_t b1 = s_b[0], b2 = s_b[1], a10 = ak[0];
+  Fe v1mk = Fe();  // POLY: v_1 of a marker-only chunk, b_1 + a_{1,0} mod p
+  if constexpr (POLY) {
+    Acc x;
+    acc_zero(x);
+    acc_add_word(x, b1);
+    acc_add_word(x, a10);
+    v1mk = acc_reduce(x);
+  }
   const uint32_t a1_s = smem_u32(s_a1);
   const uint32_t stg_s = smem_u32(stg);
 
@@ -937,7 +981,8 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     const uint64_t nbytes = ((sa + B + 15) & ~(uint64_t)15) - A;
     const uint64_t T1 = (B / W + 1 + 127) / 128;           // level-1 blocks
     uint32_t nt = (uint32_t)((T1 + CPI - 1) / CPI);
-    const bool fold = nt > 1 && (uint64_t)(nt - 1) * kWTile >= nbytes && ((T1 - 1) & 127) != 0;
+    // (POLY: the last chunk is at position 127 of its virtual node, never opening one)
+    const bool fold = nt > 1 && (uint64_t)(nt - 1) * kWTile >= nbytes && (POLY || ((T1 - 1) & 127) != 0);
     return fold ? (nt - 1) | 0x80000000u : nt;
   };
 
@@ -1060,6 +1105,11 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   Acc acc2;
   acc_zero(acc2);
   Fe root = Fe();
+  Acc pacc, acc2b;                                 // POLY: sum of weighted node values;
+  acc_zero(pacc);                                  //   next virtual node's level-2 sum
+  acc_zero(acc2b);
+  uint32_t dsh = 0;                                // POLY: d = (-C) mod 128
+  uint64_t Qp = 0;                                 // POLY: number of virtual nodes
   uint32_t cq = 0, cph = 0;                        // consumer slot and phase
   while (consumed < issued) {
     const int q = (int)cq;
@@ -1080,7 +1130,14 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       T1 = (tlast + 1 + 127) / 128;
       leff = tlast == 0 ? 0 : T1 == 1 ? 1 : T1 <= 128 ? 2 : levels_of(tlast + 1);
       acc_zero(acc2);
-      if (leff >= 3 && lane == 0) {                  // streaming state for levels >= 3
+      if constexpr (POLY) {
+        dsh = (uint32_t)((128 - T1 % 128) % 128);
+        Qp = (T1 + dsh) / 128;
+        acc_zero(pacc);
+        acc_zero(acc2b);
+        leff = 2;                                    // (no level stack)
+      }
+      if (!POLY && leff >= 3 && lane == 0) {                  // streaming state for levels >= 3
         const Geom gm = make_geom(tlast + 1);
         for (int j = 0; j <= (int)kL; j++) stk->T[j] = gm.T[j];
         for (int j = 0; j < (int)kL - 2; j++) {
@@ -1181,6 +1238,10 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     consumed++;
     produce();
 #endif
+    // POLY: virtual node of the tile's first chunk, and whether the tile crosses
+    // into the next one (virtual node boundaries fall inside tiles when d > 0)
+    const uint64_t qf = (c0 + dsh) >> 7;
+    const bool cross = POLY && ((c0 + CPI - 1 + dsh) >> 7) != qf;
     // ---- combine the 8 lanes of each group, fold into level 2 ----
 #pragma unroll
     for (int cs = 0; cs < CPG; cs++) {
@@ -1192,7 +1253,17 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       }
       const uint64_t c = c0 + (uint64_t)g * CPG + cs;
       acc_add_word(x, b1);                          // Eq. (1): b_1 + sum a s
-      if (leff == 1) {
+      if constexpr (POLY) {
+        if (c < T1) {                               // W[(c + d) mod 128] * v_1(c), v_1 reduced
+          const uint32_t wi = (uint32_t)(c + dsh) & 127;
+          const uint64_t w2[2] = {s_a2[wi], s_mkhi[wi]};
+          Fe w;
+          fe_load(w2, w);
+          const Fe v1 = acc_reduce(x);
+          if (cross && ((c + dsh) >> 7) != qf) acc_mac_fe_full(acc2b, w, v1);
+          else acc_mac_fe_full(acc2, w, v1);
+        }
+      } else if (leff == 1) {
         if (c == 0) root = acc_reduce(x);           // the whole tree is one block
       } else if (c < T1) {
         acc_mac_partial(acc2, s_a2[c & 127], x);    // a_{2, c mod 128} * v_1(c), v_1 3->2-reduced
@@ -1201,13 +1272,45 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     if (fold && lane == 0) {
       // marker-only last block c = T1 - 1 (sigma = 1, 0, ..., 0): its term
       // a_{2,c mod 128} (b_1 + a_{1,0}) mod p is key-only, precomputed per block
-      const uint64_t w2[2] = {s_mklo[(T1 - 1) & 127], s_mkhi[(T1 - 1) & 127]};
-      Fe m;
-      fe_load(w2, m);
-      acc_add_fe(acc2, m);
+      // (POLY: W[127] v_1, the chunk being at position 127)
+      if constexpr (POLY) {
+        const uint64_t w2[2] = {s_a2[127], s_mkhi[127]};
+        Fe w;
+        fe_load(w2, w);
+        if (cross && ((T1 - 1 + dsh) >> 7) != qf) acc_mac_fe_full(acc2b, w, v1mk);
+        else acc_mac_fe_full(acc2, w, v1mk);
+      } else {
+        const uint64_t w2[2] = {s_mklo[(T1 - 1) & 127], s_mkhi[(T1 - 1) & 127]};
+        Fe m;
+        fe_load(w2, m);
+        acc_add_fe(acc2, m);
+      }
     }
     // ---- close a level-2 node every 128 blocks and at the end of the string
     const uint64_t cend = fold ? T1 : c0 + CPI;
+    if constexpr (POLY) {
+      // virtual nodes completed by this tile: qf when cend + d reaches its end,
+      // and qf + 1 too at the end of the string (cend + d = 128 Q there)
+      const uint64_t cv = min(cend, T1) + dsh;
+      for (uint64_t qn = qf; qn < Qp && cv >= 128 * (qn + 1); qn++) {
+        Acc x = acc2;
+#pragma unroll
+        for (int m = 8; m < 32; m <<= 1) {
+          Acc y = acc_shfl_xor(x, m);
+          acc_add(x, y);
+        }
+        acc2 = acc2b;
+        acc_zero(acc2b);
+        Fe nv = acc_reduce(x);                      // node sum, weighted by R^(Q-1-q)
+        if (qn + 1 < Qp) nv = fe_mul(nv, poly_pow_R<BITS>(keys, Qp - 1 - qn));
+        acc_add_fe(pacc, nv);
+      }
+      if (cend >= T1 && lane == 0) {
+        acc_add_word(pacc, b2);                     // V = b_2 + sum (reading Q19)
+        emit<BITS>(os, si, acc_reduce_lo(pacc));
+      }
+      continue;
+    }
     if (leff >= 2 && ((cend & 127) == 0 || cend >= T1)) {
       Acc x = acc2;
 #pragma unroll

@@ -20,10 +20,8 @@
 
 namespace pmp {
 
-constexpr uint32_t kPolyW = kL + kL * kM;    // blob word offset of W[0..128) (lo, hi pairs)
-constexpr uint32_t kPolyLadder = 48;         // R^(2^k), k < 48 (Q' < 2^42 for T < 2^56)
-constexpr uint32_t kPolyRP = kPolyW + 2 * kM;
-constexpr uint32_t kBlobWords = kPolyRP + 2 * kPolyLadder;
+// (kPolyW, kPolyRP, kBlobWords and poly_pow_R live in pmp_kernels.cuh, shared
+// with the batch pipeline k_wstring<BITS, true>.)
 
 // W[i] = r^(128-i), RP[k] = R^(2^k) with R = r^128 = W[0].  One thread.
 template <int BITS>
@@ -42,21 +40,6 @@ __global__ void k_poly_setup(uint64_t *blob) {
     fe_store(blob + kPolyRP + 2 * k, x);
     x = fe_mul(x, x);
   }
-}
-
-// R^e from the ladder (one thread)
-template <int BITS>
-PMP_DI typename Tr<BITS>::Fe poly_pow_R(const uint64_t *__restrict__ keys, uint64_t e) {
-  using Fe = typename Tr<BITS>::Fe;
-  Fe w = fe_from_word(1, (Fe *)nullptr);
-  for (uint32_t k = 0; e; k++, e >>= 1) {
-    if (e & 1) {
-      Fe f;
-      fe_load(keys + kPolyRP + 2 * k, f);
-      w = fe_mul(w, f);
-    }
-  }
-  return w;
 }
 
 // Warp: sum over virtual nodes q' in [qf, ql] of R^(Q'-1-q') * (node sum over
@@ -162,73 +145,6 @@ k_poly_sum(const uint64_t *__restrict__ keys, const uint64_t *__restrict__ parts
     store_digest<BITS>(out, 0, fe_lo(acc_reduce(t)));
   } else {
     fe_store((uint64_t *)out, acc_reduce(t));
-  }
-}
-
-// Batch strings longer than kShortMax (the work list k_short<BITS, true>
-// leaves): warp per string.  Big strings (listed from the back) are claimed
-// dynamically first; mid strings are strided statically over the warps with
-// the next string's offsets loaded before the current one is hashed.
-template <int BITS>
-PMP_DI void poly_string(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes, uint32_t i,
-                        uint64_t o0, uint64_t o1, const OutSpec &os, const LaneKeys<BITS> &lk, int lane) {
-  using T = Tr<BITS>;
-  const uint64_t B = o1 - o0;
-  StrView s;
-  s.base = bytes + o0;
-  s.g0 = 0;
-  s.avail_end = B;
-  s.B = B;
-  s.delta = (uint32_t)((uintptr_t)(bytes + o0) & 15);
-  const uint64_t C = (B / T::W + 1 + 127) / 128;
-  const uint32_t d = (uint32_t)((128 - C % 128) % 128);
-  typename T::Acc x = poly_nodes<BITS>(keys, s, 0, C, C, 0, (C + d) / 128, 1, lk, lane);
-  if (lane == 0) {
-    acc_add_word(x, keys[1]);
-    emit<BITS>(os, i, fe_lo(acc_reduce(x)));
-  }
-}
-
-template <int BITS>
-__global__ void __launch_bounds__(kWWarps * 32, 4)
-k_poly_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
-               const uint64_t *__restrict__ offsets, uint64_t n, const OutSpec os,
-               const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t nmid = wcount[0], nbig = wcount[1];
-  LaneKeys<BITS> lk;
-  lk.load(keys + kL, lane & 7);
-  for (;;) {  // big strings: dynamic
-    uint32_t item = 0;
-    if (lane == 0) item = atomicAdd(&wcount[2], 1u);
-    item = __shfl_sync(FULL, item, 0);
-    if (item >= nbig) break;
-    const uint32_t i = wlist[n - 1 - item];
-    poly_string<BITS>(keys, bytes, i, offsets[i], offsets[i + 1], os, lk, lane);
-  }
-  const uint32_t gw = blockIdx.x * kWWarps + (threadIdx.x >> 5), nw = gridDim.x * kWWarps;
-  uint32_t item = gw;
-  uint32_t i = 0;
-  uint64_t o0 = 0, o1 = 0;
-  if (item < nmid) {
-    i = wlist[item];
-    o0 = offsets[i];
-    o1 = offsets[i + 1];
-  }
-  while (item < nmid) {  // mid strings: static stride, offsets one string ahead
-    const uint32_t nitem = item + nw;
-    uint32_t ni = 0;
-    uint64_t no0 = 0, no1 = 0;
-    if (nitem < nmid) {
-      ni = wlist[nitem];
-      no0 = offsets[ni];
-      no1 = offsets[ni + 1];
-    }
-    poly_string<BITS>(keys, bytes, i, o0, o1, os, lk, lane);
-    item = nitem;
-    i = ni;
-    o0 = no0;
-    o1 = no1;
   }
 }
 
