@@ -121,6 +121,27 @@ int pmp_hash_batch_buckets(const pmp_keys *keys, const uint8_t *bytes, const uin
                            uint64_t n, uint32_t M, uint32_t *buckets, uint32_t *counts,
                            struct CUstream_st *stream);
 
+/* Host-resident batch (the e2e path): the same digests as pmp_hash_batch for
+ * bytes / offsets / outs in HOST memory, under nkeys key schedules at once
+ * (1 <= nkeys <= PMP_HOST_MAX_KEYS; e.g. a 64-bit and a 32-bit schedule, all on
+ * one device).  The library cuts the batch into string-aligned pieces of about
+ * piece_bytes payload bytes (0: 64 MiB; a longer string is a piece alone) and
+ * streams them through the device on internal streams: the host->device copy
+ * of one piece, the hashing of the previous one and the device->host copy of
+ * the one before overlap.  Host buffers should be page-locked
+ * (cudaHostAlloc / cudaHostRegister) for the copies to run asynchronously.
+ *   bytes   (host) payload, string i = bytes[offsets[i], offsets[i+1]);
+ *   offsets (host) n+1 uint64, non-decreasing;
+ *   outs[k] (host) n digests for keys[k] (uint64 / uint32 by its width).
+ * Stream-ordered like every call: the pieces start after prior work on
+ * `stream`, and the digests are in host memory once `stream` has reached this
+ * point (synchronise it before reading outs); the host buffers must stay
+ * valid until then.  Device scratch is stream-ordered and released by then.
+ * Errors as pmp_hash_batch, and PMP_EINVAL for keys on different devices. */
+#define PMP_HOST_MAX_KEYS 4
+int pmp_hash_batch_host(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
+                        uint64_t n, void *const *outs, uint64_t piece_bytes, struct CUstream_st *stream);
+
 /* Hash one string of `len` bytes at `bytes` (device, any alignment); writes
  * one digest (uint64 / uint32) to `out` (device).  Block-parallel over the
  * level-2 nodes of the tree (128 level-1 blocks each), then one launch per

@@ -51,6 +51,7 @@ def lib() -> ctypes.CDLL:
             "pmp_keys_free": ([_vp], None),
             "pmp_hash_batch": ([_vp, _vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_batch_buckets": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _vp, _vp], _int),
+            "pmp_hash_batch_host": ([_vp, _int, _vp, _vp, _u64, _vp, _u64, _vp], _int),
             "pmp_hash_long": ([_vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_long_partial": ([_vp, _vp, _u64, _u64, _u64, _vp, _vp], _int),
             "pmp_hash_long_combine": ([_vp, _vp, _int, _u64, _vp, _vp], _int),
@@ -123,6 +124,14 @@ def pmp_keys_free(keys: int) -> None:
 
 def pmp_hash_batch(keys: int, bytes_ptr: int, offsets_ptr: int, n: int, out_ptr: int, stream: int) -> int:
     return lib().pmp_hash_batch(keys, bytes_ptr, offsets_ptr, n, out_ptr, stream)
+
+
+def pmp_hash_batch_host(keys: list, bytes_ptr: int, offsets_ptr: int, n: int, out_ptrs: list,
+                        piece_bytes: int, stream: int) -> int:
+    """keys: list of pmp_keys* handles; out_ptrs: one host digest buffer per key."""
+    ka = (_vp * len(keys))(*keys)
+    oa = (_vp * len(out_ptrs))(*out_ptrs)
+    return lib().pmp_hash_batch_host(ka, len(keys), bytes_ptr, offsets_ptr, n, oa, piece_bytes, stream)
 
 
 def pmp_hash_batch_buckets(keys: int, bytes_ptr: int, offsets_ptr: int, n: int, M: int, buckets_ptr: int,
@@ -290,6 +299,28 @@ def hash_batch(keys: Keys, payload, offsets, out=None, stream=None):
     _check(pmp_hash_batch(keys.handle, payload.data_ptr(), offsets.data_ptr(), max(n, 0),
                           out.data_ptr(), _stream_ptr(stream)), "pmp_hash_batch")
     return out
+
+
+def hash_batch_host(keys: list, payload, offsets, outs=None, piece_bytes: int = 0):
+    """Host-resident batch (numpy uint8 payload, uint64 offsets, or pinned torch
+    CPU tensors) under one or more key schedules; returns one host digest array
+    per key.  Pieces stream through the device with copy/compute overlap
+    (pmp_hash_batch_host); this wrapper waits for the digests."""
+    import numpy as np
+
+    def ptr(a):
+        return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+    n = (offsets.numel() if hasattr(offsets, "numel") else offsets.size) - 1
+    if outs is None:
+        outs = [np.empty(max(n, 0), dtype=np.uint64 if k.bits == 64 else np.uint32) for k in keys]
+    import torch
+
+    st = torch.cuda.current_stream()
+    _check(pmp_hash_batch_host([k.handle for k in keys], ptr(payload), ptr(offsets), max(n, 0),
+                               [ptr(o) for o in outs], piece_bytes, int(st.cuda_stream)), "pmp_hash_batch_host")
+    st.synchronize()
+    return outs
 
 
 def hash_batch_buckets(keys: Keys, payload, offsets, M: int, counts=None, out=None, stream=None):

@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // pmp_api.cu -- libpmp.so: the C ABI declared in include/pmp.h.
 //
 // Host side of the PM+ path: key generation (project contract, reading Q12),
@@ -11,6 +13,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -652,10 +655,12 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   const ParamKeys pk = param_keys(k);
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(k_short<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
-    cudaFuncSetAttribute(k_short<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
-    cudaFuncSetAttribute(k_short<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
-    cudaFuncSetAttribute(k_short<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
+    const void *fs[4] = {(const void *)k_short<64>, (const void *)k_short<32>, (const void *)k_short<64, true>,
+                         (const void *)k_short<32, true>};
+    for (const void *f : fs) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    }
   });
   // the offsets ring is fed by TMA bulk copies, which need 16-byte aligned sources
   if ((uintptr_t)offsets & 15) {
@@ -667,10 +672,19 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     offsets = (const uint64_t *)al;
   }
   uint64_t grid = (n + kTile - 1) / kTile;
-  const uint64_t per_sm = (228u * 1024u) / (kShortSmem + 1024u);  // resident blocks per SM (smem bound)
-  const uint64_t maxgrid = (uint64_t)sms * (per_sm ? per_sm : 1);  // persistent grid
-  if (grid > maxgrid) grid = maxgrid;
   const int threads = (kShortWarps + 1) * 32;  // + producer warp
+  static int sper_sm[2][2] = {{0, 0}, {0, 0}};   // resident blocks per SM [v2][64-bit]
+  int &sps = sper_sm[v2][k->bits == 64];
+  if (sps == 0) {
+    if (v2)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sps, k->bits == 64 ? (const void *)k_short<64, true> : (const void *)k_short<32, true>, threads, kShortSmem);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sps, k->bits == 64 ? (const void *)k_short<64> : (const void *)k_short<32>, threads, kShortSmem);
+    if (sps < 1) sps = 1;
+    if (getenv("PMP_VERBOSE")) fprintf(stderr, "pmp: k_short smem %zu B, %d blocks/SM\n", kShortSmem, sps);
+  }
+  const uint64_t maxgrid = (uint64_t)sms * sps;  // persistent grid
+  if (grid > maxgrid) grid = maxgrid;
   int rc;
   if (v2) {  // two-level variant (8(f4)): short strings in k_short, the rest warp per string
     if (k->bits == 64)
@@ -717,6 +731,7 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wps, k_wstring<32>, kWBlockWarps * 32, kWSmem);
     if (wps < 1) wps = 1;
+    if (getenv("PMP_VERBOSE")) fprintf(stderr, "pmp: k_wstring smem %zu B, %d blocks/SM\n", kWSmem, wps);
   }
   const unsigned wgrid = (unsigned)(sms * wps);
   if (k->bits == 64)
@@ -743,6 +758,102 @@ int pmp_hash_batch_buckets(const pmp_keys *k, const uint8_t *bytes, const uint64
   os.M = M;
   os.counts = counts;
   return hash_batch_impl(k, bytes, offsets, n, os, st);
+}
+
+// Host-resident batches: string-aligned pieces streamed through the device on
+// kHostSlots internal streams, so that the host->device copy of one piece, the
+// hashing of another and the device->host copy of a third overlap (the copy
+// engines of both directions and the SMs work at once).
+namespace {
+constexpr int kHostSlots = 3;
+struct HostStreams {
+  bool init = false;
+  cudaStream_t st[kHostSlots];
+};
+HostStreams g_host_st[64];
+}  // namespace
+
+int pmp_hash_batch_host(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
+                        uint64_t n, void *const *outs, uint64_t piece_bytes, cudaStream_t stream) {
+  if (!keys || !outs || nkeys < 1 || nkeys > PMP_HOST_MAX_KEYS) return PMP_EINVAL;
+  if (n == 0) return 0;
+  if (!bytes || !offsets || n >= (1ULL << 32)) return PMP_EINVAL;
+  for (int k = 0; k < nkeys; k++) {
+    if (!keys[k] || !outs[k]) return PMP_EINVAL;
+    if (int rc = check_keys(keys[k])) return rc;
+    if (keys[k]->device != keys[0]->device) return PMP_EINVAL;
+  }
+  const int dev = keys[0]->device;
+  if (dev < 0 || dev >= 64) return PMP_EINVAL;
+  if (piece_bytes == 0) piece_bytes = 64ull << 20;
+  // string-aligned pieces of <= piece_bytes payload (a longer string is a piece alone)
+  std::vector<uint64_t> cut{0};
+  uint64_t max_span = 0, max_cnt = 0;
+  while (cut.back() < n) {
+    const uint64_t s0 = cut.back();
+    const uint64_t *e = std::upper_bound(offsets + s0 + 1, offsets + n + 1, offsets[s0] + piece_bytes);
+    uint64_t s1 = (uint64_t)(e - offsets) - 1;
+    if (s1 <= s0) s1 = s0 + 1;
+    cut.push_back(s1);
+    max_span = std::max(max_span, offsets[s1] - offsets[s0]);
+    max_cnt = std::max(max_cnt, s1 - s0);
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_host_st[dev].init) {
+      for (int q = 0; q < kHostSlots; q++) cudaStreamCreateWithFlags(&g_host_st[dev].st[q], cudaStreamNonBlocking);
+      g_host_st[dev].init = true;
+    }
+  }
+  cudaStream_t *st = g_host_st[dev].st;
+  // stream order: the pieces start after prior work on `stream`, and later work on
+  // `stream` starts after every piece's digests are in host memory
+  cudaEvent_t ev_in = nullptr, ev_out[kHostSlots] = {nullptr, nullptr, nullptr};
+  if (cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess) return PMP_ECUDA;
+  cudaEventRecord(ev_in, stream);
+  for (int q = 0; q < kHostSlots; q++) cudaStreamWaitEvent(st[q], ev_in, 0);
+  cudaEventDestroy(ev_in);
+  // per slot: payload (+16 B alignment shift, +32 B tail for whole 16-byte units), offsets, digests per key
+  const size_t cap_b = (size_t)max_span + 48, cap_o = (size_t)(max_cnt + 1) * 8, cap_d = (size_t)max_cnt * 8;
+  const size_t slot_bytes = ((cap_b + 255) & ~(size_t)255) + ((cap_o + 255) & ~(size_t)255) + (size_t)nkeys * ((cap_d + 255) & ~(size_t)255);
+  uint8_t *slot[kHostSlots] = {nullptr, nullptr, nullptr};
+  int rc = 0;
+  for (int q = 0; q < kHostSlots && !rc; q++)
+    if (cudaMallocAsync((void **)&slot[q], slot_bytes, st[q]) != cudaSuccess) rc = PMP_ENOMEM;
+  for (size_t p = 0; p + 1 < cut.size() && !rc; p++) {
+    const int q = (int)(p % kHostSlots);
+    const uint64_t s0 = cut[p], s1 = cut[p + 1], cnt = s1 - s0;
+    uint8_t *d_b = slot[q];
+    uint64_t *d_o = (uint64_t *)(slot[q] + ((cap_b + 255) & ~(size_t)255));
+    uint8_t *d_d = (uint8_t *)d_o + ((cap_o + 255) & ~(size_t)255);
+    const uint64_t b0 = offsets[s0], nb = offsets[s1] - b0, sh = b0 & 15;
+    // the kernels address string i at bytes + offsets[i]: keep the global offsets and
+    // shift the base (same 16-byte phase as the host copy, so units stay aligned)
+    const uint8_t *d_base = d_b + sh - b0;
+    if (nb && cudaMemcpyAsync(d_b + sh, bytes + b0, nb, cudaMemcpyHostToDevice, st[q]) != cudaSuccess) rc = PMP_ECUDA;
+    if (!rc && cudaMemcpyAsync(d_o, offsets + s0, (cnt + 1) * 8, cudaMemcpyHostToDevice, st[q]) != cudaSuccess)
+      rc = PMP_ECUDA;
+    for (int k = 0; k < nkeys && !rc; k++) {
+      const size_t w = keys[k]->bits / 8;
+      uint8_t *d_out = d_d + (size_t)k * ((cap_d + 255) & ~(size_t)255);
+      rc = pmp_hash_batch(keys[k], d_base, d_o, cnt, d_out, st[q]);
+      if (!rc && cudaMemcpyAsync((uint8_t *)outs[k] + s0 * w, d_out, cnt * w, cudaMemcpyDeviceToHost, st[q]) !=
+                     cudaSuccess)
+        rc = PMP_ECUDA;
+    }
+  }
+  for (int q = 0; q < kHostSlots; q++) {
+    if (slot[q]) cudaFreeAsync(slot[q], st[q]);
+    if (cudaEventCreateWithFlags(&ev_out[q], cudaEventDisableTiming) != cudaSuccess) {
+      if (!rc) rc = PMP_ECUDA;
+      continue;
+    }
+    cudaEventRecord(ev_out[q], st[q]);
+    cudaStreamWaitEvent(stream, ev_out[q], 0);
+    cudaEventDestroy(ev_out[q]);
+  }
+  if (!rc && cudaGetLastError() != cudaSuccess) rc = PMP_ECUDA;
+  return rc;
 }
 
 int pmp_hash_long_partial(const pmp_keys *k, const uint8_t *local, uint64_t local_len, uint64_t g0,

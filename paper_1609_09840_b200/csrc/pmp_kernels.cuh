@@ -378,7 +378,10 @@ PMP_DI void mbar_arrive(uint64_t *bar) {
 // consumers to the work list of k_wstring in either mode.
 constexpr int kPasses = 1;                                     // strings per consumer lane per tile
 constexpr int kTile = 32 * kShortWarps * kPasses;              // 384
-constexpr int kRing = 8, kOffAhead = 4;
+#ifndef PMP_SHORT_SLOTS
+#define PMP_SHORT_SLOTS 8
+#endif
+constexpr int kRing = PMP_SHORT_SLOTS, kOffAhead = PMP_SHORT_SLOTS / 2;  // tile slots (power of 2), offsets prefetch
 constexpr uint32_t kByteRing = PMP_SHORT_RING_KB * 1024;
 // Block-wide counting sort of each tile by word count before hashing
 // (PMP_SHORT_SORT=1): removes most of the zero-padding multiply-adds but costs
@@ -387,7 +390,7 @@ constexpr uint32_t kByteRing = PMP_SHORT_RING_KB * 1024;
 #ifndef PMP_SHORT_SORT
 #define PMP_SHORT_SORT 0
 #endif
-constexpr uint32_t kSpanMaxTile = 32 * 1024;                   // larger spans go direct
+constexpr uint32_t kSpanMaxTile = kByteRing / 2 < 32 * 1024 ? kByteRing / 2 : 32 * 1024;  // larger spans go direct
 constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
 constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
 struct TileHdr {
@@ -397,7 +400,7 @@ struct TileHdr {
 };
 constexpr size_t kShortSmem = 256 /* keys */ + kByteRing + kSlack + 16 + (size_t)kRing * kOffBytes +
                               (size_t)kRing * sizeof(TileHdr) +
-                              (size_t)(3 * kRing) * 8 + 256 /* sort histograms */ + 2 * kTile /* sort permutation */ + 128;
+                              (size_t)(3 * kRing) * 8 + (PMP_SHORT_SORT ? 256 /* sort histograms */ + 2 * kTile /* permutation */ : 0) + 128;
 
 template <int BITS, bool V2 = false>
 __global__ void __launch_bounds__((kShortWarps + 1) * 32)
@@ -890,14 +893,328 @@ struct WHdr {        // one per stage, written by the issuing lane
   uint32_t nt;       // tiles | fold flag << 31
   uint32_t nb;       // bytes copied (0: the tile holds only a marker-only block)
 };
-constexpr size_t kWSmemPerWarp =
+constexpr size_t kWSmemPerWarpBig =
     ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + 15) & ~(size_t)15;
+constexpr size_t kWSmemPerWarpMid =   // mid_phase's layout (kept in step with kMSmemPerWarp)
+    ((size_t)2 * (4 * (1024 + 32) + 4 * 32 + 8) + 15) & ~(size_t)15;
+constexpr size_t kWSmemPerWarp = kWSmemPerWarpBig > kWSmemPerWarpMid ? kWSmemPerWarpBig : kWSmemPerWarpMid;
 // block region: a_{2,0..127} (POLY: W[0..127] lo words), b_1..8, the key-only
 // values a_{2,r} * (b_1 + a_{1,0}) mod p (lo words, then hi bits) of a
 // marker-only level-1 block at position r (POLY: lo words unused, hi words =
 // W hi bits), a_{1,0..127}
 constexpr size_t kWBlockRegion = 1024 + 64 + 1024 + 512 + 1024 /* a_{1,0..127} */;
 constexpr size_t kWSmem = kWBlockRegion + kWBlockWarps * kWSmemPerWarp;
+
+// Mid strings in 8-lane groups (mid_phase) instead of warp per string.
+#ifndef PMP_MID_GROUPS
+#define PMP_MID_GROUPS 1
+#endif
+// ============================================================= mid strings (k_wstring, second phase)
+// Mid strings (kShortMax < B < kBigBytes, listed at the front of the work
+// list).  Such a string has T1 <= 128 level-1 blocks, so its tree is one block
+// (L_eff = 1) or one level-2 node (L_eff = 2) and needs no level stack.  One
+// 8-lane group hashes one string, four strings per warp: lane r of group g
+// owns units r, r+8, ..., r+56 of the group's 1 KiB piece (one PM+64 block,
+// two PM+32 blocks) per iteration, the 8 lanes combine their exact sums with 3
+// in-group shuffle levels (every lane ends with the block value), and the
+// level-2 sum is kept redundantly by all 8 lanes -- so closing a string needs
+// no shuffle at all, and the per-string control (geometry, the level-2 close,
+// the digest) is paid once per warp for four strings.
+// Each iteration stages the four groups' 1 KiB pieces in one ring slot (four
+// TMA bulk copies completing on one mbarrier).  Work: the warp claims batches
+// of 32 strings (one atomic, one string per lane) and hands them to its
+// groups as they finish, so a group that drew short strings takes more.
+// POLY (reading Q19): C = T1 <= 128 gives Q = 1 virtual node, d = 128 - C,
+// and chunk c weighs W[c + d] = r^(C - c); every string (T1 = 1 included)
+// gets V = b_2 + sum.
+constexpr int kMPiece = 1024;                  // bytes per group per iteration
+constexpr int kMSlot = kMPiece + 32;           // + 16 B overlap + 16 B read slack
+#ifndef PMP_M_STAGES
+#define PMP_M_STAGES 2
+#endif
+constexpr int kMStages = PMP_M_STAGES;
+struct MHdr {        // per stage and group, written by the group's leader
+  uint64_t sa;       // address of the string's byte 0
+  uint64_t B;        // length
+  uint32_t i;        // string index
+  uint32_t t;        // piece index within the string
+  uint32_t nt;       // pieces | fold << 31 (0: group idle this iteration)
+  uint32_t nb;       // bytes copied
+};
+constexpr size_t kMSmemPerWarp = ((size_t)kMStages * (4 * kMSlot + 4 * sizeof(MHdr) + 8) + 15) & ~(size_t)15;
+
+// Runs after the warp has drained its big strings; uses the warp's shared
+// region (wbase) with its own ring layout and barriers.
+template <int BITS, bool POLY>
+__device__ __noinline__ void mid_phase(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
+                                       const uint64_t *__restrict__ offsets, const OutSpec &os,
+                                       const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount,
+                                       uint32_t nmid, const uint64_t *s_a2, const uint64_t *s_mklo,
+                                       const uint32_t *s_mkhi, const uint64_t *s_a1, uint64_t b1, uint64_t b2,
+                                       typename Tr<BITS>::Fe v1mk, uint8_t *wbase) {
+  using T = Tr<BITS>;
+  using Acc = typename T::Acc;
+  using Fe = typename T::Fe;
+  constexpr int CPG = T::CPG, W = T::W;
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 3, r = lane & 7;
+  const bool leader = r == 0;
+  MHdr *hdr = reinterpret_cast<MHdr *>(wbase + (size_t)kMStages * 4 * kMSlot);   // [stage][group]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(hdr + 4 * kMStages);
+  if (nmid == 0) return;
+  if (lane == 0) {
+    for (int q = 0; q < kMStages; q++) mbar_init(&bar[q], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  const uint32_t a1_s = smem_u32(s_a1);
+  const uint32_t stg_s = smem_u32(wbase);
+
+  // ---- work: batches of 32 strings per warp (lane e holds string e), two
+  // batches in registers (cur is being handed out, nxt is in flight)
+  uint32_t cur_i = 0, nxt_i = 0, bi = 0, cur_n = 0, nxt_n = 0;
+  uint64_t cur_o0 = 0, cur_o1 = 0, nxt_o0 = 0, nxt_o1 = 0;
+  auto fetch_batch = [&]() {  // -> nxt
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&wcount[3], 32u);
+    base = __shfl_sync(FULL, base, 0);
+    nxt_n = base < nmid ? min(32u, nmid - base) : 0u;
+    if ((uint32_t)lane < nxt_n) {
+      nxt_i = wlist[base + lane];
+      nxt_o0 = offsets[nxt_i];
+      nxt_o1 = offsets[nxt_i + 1];
+    }
+  };
+  fetch_batch();
+  cur_i = nxt_i;
+  cur_o0 = nxt_o0;
+  cur_o1 = nxt_o1;
+  cur_n = nxt_n;
+  if (cur_n) fetch_batch();
+
+  // ---- issue side: a cursor per group (replicated in its 8 lanes)
+  uint64_t p_sa = 0, p_B = 0;
+  uint32_t p_i = 0, p_t = 0, p_nt = 0;
+  bool p_have = false, p_done = false;
+  uint32_t issued = 0, consumed = 0, pq = 0;
+  auto pieces_of = [&](uint64_t B) -> uint32_t {
+    const uint64_t T1 = (B / W + 1 + 127) / 128;
+    const uint32_t nt = (uint32_t)((T1 + CPG - 1) / CPG);
+    // a trailing piece holding only the marker-only block is folded away
+    const bool fold = nt > 1 && (uint64_t)(nt - 1) * kMPiece >= B;
+    return fold ? (nt - 1) | 0x80000000u : nt;
+  };
+  auto produce = [&]() {
+    while (!p_done && issued - consumed < (uint32_t)kMStages) {
+      // groups that need a string take the next ones of the batch, in group order
+      const bool need = !p_have || p_t == (p_nt & 0x7fffffffu);
+      const unsigned needm = __ballot_sync(FULL, need && leader);
+      if (needm) {
+        const uint32_t rank = __popc(needm & ((1u << lane) - 1));  // meaningful in leaders
+        const uint32_t nneed = __popc(needm);
+        const uint32_t avail = cur_n > bi ? cur_n - bi : 0u;
+        const uint32_t rk = __shfl_sync(FULL, rank, lane & ~7);     // the group's rank
+        const bool from_cur = rk < avail;
+        const int src = (int)(from_cur ? bi + rk : rk - avail);
+        const uint64_t c0 = __shfl_sync(FULL, cur_o0, src & 31), c1 = __shfl_sync(FULL, cur_o1, src & 31);
+        const uint64_t n0 = __shfl_sync(FULL, nxt_o0, src & 31), n1 = __shfl_sync(FULL, nxt_o1, src & 31);
+        const uint32_t ci = __shfl_sync(FULL, cur_i, src & 31), ni = __shfl_sync(FULL, nxt_i, src & 31);
+        if (need) {
+          const bool ok = from_cur || (uint32_t)src < nxt_n;
+          p_have = ok;
+          if (ok) {
+            const uint64_t o0 = from_cur ? c0 : n0, o1 = from_cur ? c1 : n1;
+            p_sa = (uint64_t)(uintptr_t)(bytes + o0);
+            p_B = o1 - o0;
+            p_i = from_cur ? ci : ni;
+            p_nt = pieces_of(p_B);
+            p_t = 0;
+          }
+        }
+        if (cur_n && nneed >= avail) {  // batch used up: rotate (nxt may be empty)
+          bi = min(nneed - avail, nxt_n);
+          cur_i = nxt_i;
+          cur_o0 = nxt_o0;
+          cur_o1 = nxt_o1;
+          cur_n = nxt_n;
+          if (cur_n) fetch_batch();
+          else nxt_n = 0;
+        } else if (cur_n) {
+          bi += nneed;
+        }
+      }
+      if (!__any_sync(FULL, p_have)) {
+        p_done = true;
+        break;
+      }
+      // stage pq: this group's piece p_t
+      uint32_t nb = 0;
+      const uint64_t A = p_sa & ~(uint64_t)15;
+      const uint64_t off = (uint64_t)p_t * kMPiece;
+      if (p_have) {
+        const uint64_t nbytes = ((p_sa + p_B + 15) & ~(uint64_t)15) - A;
+        nb = off < nbytes ? (uint32_t)min((uint64_t)(kMPiece + 16), nbytes - off) : 0u;
+      }
+      const uint32_t tot = __reduce_add_sync(FULL, leader ? nb : 0u);
+      MHdr &h = hdr[pq * 4 + g];
+      if (leader) {
+        h.sa = p_sa;
+        h.B = p_B;
+        h.i = p_i;
+        h.t = p_t;
+        h.nt = p_have ? p_nt : 0u;
+        h.nb = nb;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the slot
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_tx(&bar[pq], tot);
+      __syncwarp();
+      if (leader && nb)
+        bulk_g2s(wbase + (size_t)(pq * 4 + g) * kMSlot, reinterpret_cast<const void *>(A + off), nb, &bar[pq]);
+      if (p_have) p_t++;
+      pq = pq + 1 == (uint32_t)kMStages ? 0u : pq + 1;
+      issued++;
+    }
+  };
+  produce();
+
+  // ---- consumer: per group, the level-2 sum of the string being hashed
+  Acc acc2;
+  acc_zero(acc2);
+  uint32_t cq = 0, cph = 0;
+  while (consumed < issued) {
+    const int q = (int)cq;
+    mbar_wait(&bar[q], cph);
+    if (++cq == (uint32_t)kMStages) {
+      cq = 0;
+      cph ^= 1;
+    }
+    const MHdr &h = hdr[q * 4 + g];
+    const uint32_t ntf = h.nt, t = h.t, si = h.i;
+    const uint64_t B = h.B;
+    const uint32_t delta = (uint32_t)h.sa & 15u;
+    const bool active = ntf != 0;
+    const uint32_t nt = ntf & 0x7fffffffu;
+    const bool last = active && t + 1 == nt;
+    const bool fold = last && (ntf >> 31);
+    const uint64_t tlast = B / W;                   // marker word index
+    const uint32_t rbytes = (uint32_t)(B % W);
+    const uint64_t T1 = (tlast + 1 + 127) / 128;
+    // ---- this lane's 8 units of the group's piece, realigned to the string
+    const uint32_t ub = stg_s + (uint32_t)(q * 4 + g) * kMSlot + 16 * r;
+    uint4 U[8];
+    if (__all_sync(FULL, delta == 0)) {
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(U[j].x), "=r"(U[j].y), "=r"(U[j].z), "=r"(U[j].w) : "r"(ub + 128 * j));
+    } else {
+      const uint32_t a0 = ub + (delta & ~3u), sh = 8 * (delta & 3);
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const uint32_t a = a0 + 128 * j;
+        const uint32_t y0 = lds_u32(a), y1 = lds_u32(a + 4), y2 = lds_u32(a + 8), y3 = lds_u32(a + 12),
+                       y4 = lds_u32(a + 16);
+        U[j] = make_uint4(funnel(y0, y1, sh), funnel(y1, y2, sh), funnel(y2, y3, sh), funnel(y3, y4, sh));
+      }
+    }
+    const uint64_t tw0 = (uint64_t)t * (kMPiece / W);  // first word of the piece
+    const bool has_marker = active && tlast < tw0 + kMPiece / W;
+    if (__any_sync(FULL, has_marker || !active)) {
+      if (!active) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) U[j] = make_uint4(0, 0, 0, 0);
+      } else if (has_marker) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) fixup_unit<BITS>(U[j], tw0 + (uint64_t)(16 * (r + 8 * j)) / W, tlast, rbytes);
+      }
+    }
+    // ---- level-1 multiply-accumulate
+    Acc part[CPG];
+    if constexpr (BITS == 64) {
+      MacAcc64 A;
+      macc_zero(A);
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        uint4 kk;  // a_{1,2u}, a_{1,2u+1}, u = r + 8j
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
+                     : "r"(a1_s + 16 * (r + 8 * j)));
+        mac64(A, kk.x, kk.y, U[j].x, U[j].y);
+        mac64(A, kk.z, kk.w, U[j].z, U[j].w);
+      }
+      part[0] = macc_normalize(A);
+    } else {
+      Acc3 A[2] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+      for (int jj = 0; jj < 4; jj++) {
+        uint4 kk;  // a_{1,4u..4u+3}, u = r + 8 jj, the same for both blocks
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
+                     : "r"(a1_s + 16 * (r + 8 * jj)));
+#pragma unroll
+        for (int cs = 0; cs < 2; cs++) {
+          const uint4 &u = U[jj + 4 * cs];
+          mac32(A[cs], kk.x, u.x);
+          mac32(A[cs], kk.y, u.y);
+          mac32(A[cs], kk.z, u.z);
+          mac32(A[cs], kk.w, u.w);
+        }
+      }
+      part[0] = A[0];
+      part[CPG - 1] = A[1];
+    }
+    __syncwarp();
+    consumed++;
+    produce();                                      // the slot is free: refill it
+    // ---- block values (in-group shuffles), level 2
+    if (active && t == 0) acc_zero(acc2);
+    uint64_t lo1 = 0;                               // L_eff = 1: V mod 2^n
+#pragma unroll
+    for (int cs = 0; cs < CPG; cs++) {
+      Acc x = part[cs];
+#pragma unroll
+      for (int m = 1; m < 8; m <<= 1) {
+        Acc y = acc_shfl_xor(x, m);
+        acc_add(x, y);
+      }
+      acc_add_word(x, b1);                          // Eq. (1): b_1 + sum a s
+      const uint64_t c = (uint64_t)t * CPG + cs;
+      if (active && c < T1) {
+        if constexpr (POLY) {                       // W[c + 128 - C] v_1(c)
+          const uint32_t wi = (uint32_t)(c + 128 - T1);
+          const uint64_t w2[2] = {s_a2[wi], s_mkhi[wi]};
+          Fe w;
+          fe_load(w2, w);
+          acc_mac_fe_full(acc2, w, acc_reduce(x));
+        } else if (T1 == 1) {
+          lo1 = acc_reduce_lo(x);                   // the whole tree is this block
+        } else {
+          acc_mac_partial(acc2, s_a2[c], x);        // a_{2,c} v_1(c), v_1 3->2-reduced
+        }
+      }
+    }
+    if (last) {
+      if (fold) {                                   // marker-only block T1 - 1
+        if constexpr (POLY) {
+          const uint64_t w2[2] = {s_a2[127], s_mkhi[127]};
+          Fe w;
+          fe_load(w2, w);
+          acc_mac_fe_full(acc2, w, v1mk);
+        } else {
+          const uint64_t w2[2] = {s_mklo[T1 - 1], s_mkhi[T1 - 1]};
+          Fe m;
+          fe_load(w2, m);
+          acc_add_fe(acc2, m);
+        }
+      }
+      if (POLY || T1 > 1) {
+        acc_add_word(acc2, b2);                     // b_2 (POLY: V = b_2 + sum, reading Q19)
+        lo1 = acc_reduce_lo(acc2);
+      }
+      if (leader) emit<BITS>(os, si, lo1);
+    }
+  }
+}
+
 
 #ifndef PMP_W_EARLY
 #define PMP_W_EARLY 0
@@ -1028,7 +1345,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       nxt_o1 = offsets[nxt_i + 1];
     }
   };
-  fetch_batch(0);
+  if (!PMP_MID_GROUPS) fetch_batch(0);
   // next item into (sa, B, i); false when the warp's work is exhausted
   auto next_item = [&](uint64_t &sa, uint64_t &B, uint32_t &i) -> bool {
     while (big_open) {
@@ -1041,6 +1358,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       }
       claim_step();                                   // (blocks on the pending load)
     }
+    if (PMP_MID_GROUPS) return false;                 // mid strings: mid_phase
     const uint32_t item = gw + mk * nw;
     if (item >= nmid) return false;
     const int e = (int)(mk & 31);
@@ -1350,6 +1668,15 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       if (lane == 0) emit<BITS>(os, si, fe_lo(root));
     }
   }
+#if PMP_MID_GROUPS
+  static_assert(kWSmemPerWarp >= kMSmemPerWarp, "mid_phase layout");
+  __syncwarp();
+  if (lane == 0)   // the big phase's barriers sit in memory mid_phase reuses
+    for (int q = 0; q < kWStages; q++) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar[q])) : "memory");
+  __syncwarp();
+  mid_phase<BITS, POLY>(keys, bytes, offsets, os, wlist, wcount, nmid, s_a2, s_mklo, s_mkhi, s_a1, b1, b2,
+                        v1mk, wbase);
+#endif
 }
 
 // ============================================================= long string

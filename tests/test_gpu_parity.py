@@ -182,6 +182,30 @@ def test_all_short_batch_alignments(torch_dev, oracle_lib, bits):
 
 
 @pytest.mark.parametrize("bits", [32, 64])
+@pytest.mark.parametrize("shift", [0, 5])
+def test_mid_strings_group_path(torch_dev, oracle_lib, bits, shift):
+    """Mid strings (128 B <= B < 64 KiB: one 8-lane group per string, four per
+    warp, warp batches of 32 handed out as groups finish): lengths at and around
+    every multiple of 1 KiB (marker-only trailing blocks folded), the 64 KiB
+    big-string boundary, and a log-uniform crowd so that batches rotate while
+    groups are at different points of their strings; string count not a
+    multiple of 32, short strings interleaved."""
+    rng = np.random.default_rng(bits * 10 + shift)
+    edge = [k * 1024 + d for k in range(1, 64) for d in (-1, 0, 1)] + [65535, 65536, 65537, 128, 129, 511, 512, 513]
+    crowd = np.floor(2.0 ** rng.uniform(7, 16, size=3001)).astype(np.uint64)
+    shorts = rng.integers(0, 128, size=500, dtype=np.uint64)
+    lens = np.concatenate([np.array(edge, dtype=np.uint64), crowd, shorts])
+    rng.shuffle(lens)
+    off = datagen.offsets_from_lengths(lens) + shift
+    pay = datagen.payload_host(31 + shift, 0, int(off[-1]))
+    keys = pmp.Keys.generate(31, bits)
+    got = run_batch(torch_dev, keys, pay, off)
+    want = oracle_batch(oracle_lib, 31, bits, pay, off)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, [(int(i), int(lens[i])) for i in bad[:10]]
+
+
+@pytest.mark.parametrize("bits", [32, 64])
 def test_long_strings_in_batch(torch_dev, oracle_lib, bits):
     """Warp-per-string path across level-2 (128 blocks) and level-3 (128^2 blocks)
     boundaries, misaligned starts, mixed with short strings and big ones first."""
@@ -392,3 +416,21 @@ def test_stream_reset_and_reuse(torch_dev, oracle_lib):
         with pytest.raises(pmp.PmpError):
             st.update(d, 1)
         st.reset()
+
+
+@pytest.mark.parametrize("piece", [0, 4096, 100_000])
+def test_host_batch_streaming(torch_dev, oracle_lib, piece):
+    """pmp_hash_batch_host (host-resident bytes/offsets/digests, two key
+    schedules at once) equals the device path and the oracle: pieces smaller
+    than one string (a string alone in its piece), pieces ending anywhere,
+    a batch that starts at an odd offset of its buffer."""
+    rng = np.random.default_rng(piece + 1)
+    lens = np.concatenate([rng.integers(0, 200, size=3000), [70_000, 5000, 0, 1, 127, 128, 9000]]).astype(np.uint64)
+    rng.shuffle(lens)
+    off = datagen.offsets_from_lengths(lens) + 11
+    pay = datagen.payload_host(41, 0, int(off[-1]))
+    k64, k32 = pmp.Keys.generate(41, 64), pmp.Keys.generate(42, 32)
+    got64, got32 = pmp.hash_batch_host([k64, k32], pay, off, piece_bytes=piece)
+    assert np.array_equal(got64, oracle_batch(oracle_lib, 41, 64, pay, off))
+    assert np.array_equal(got32, oracle_batch(oracle_lib, 42, 32, pay, off))
+    assert np.array_equal(got64, run_batch(torch_dev, k64, pay, off))

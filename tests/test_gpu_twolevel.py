@@ -57,6 +57,24 @@ def test_hash2_batch_length_sweep(dev, oracle_lib, bits, shift):
 
 
 @pytest.mark.parametrize("bits", [32, 64])
+def test_hash2_mid_strings_group_path(dev, oracle_lib, bits):
+    """Mid strings through the 8-lane group phase (one virtual node, weights
+    W[c + 128 - C]): lengths around every multiple of 1 KiB up to the 64 KiB
+    big-string boundary plus a log-uniform crowd, misaligned."""
+    rng = np.random.default_rng(bits + 7)
+    edge = [k * 1024 + d for k in range(1, 64) for d in (-1, 0, 1)] + [65535, 65536, 128, 129, 512, 513]
+    crowd = np.floor(2.0 ** rng.uniform(7, 16, size=1501)).astype(np.uint64)
+    lens = np.concatenate([np.array(edge, dtype=np.uint64), crowd, rng.integers(0, 128, size=200, dtype=np.uint64)])
+    rng.shuffle(lens)
+    off = datagen.offsets_from_lengths(lens) + 3
+    pay = datagen.payload_host(61, 0, int(off[-1]))
+    got = _batch(dev, pmp.Keys.generate(61, bits), pay, off)
+    want = _want(oracle_lib, oracle_lib.keygen(61, bits), pay, off)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, [(int(i), int(lens[i])) for i in bad[:10]]
+
+
+@pytest.mark.parametrize("bits", [32, 64])
 def test_hash2_batch_tiny_config_and_long_members(dev, oracle_lib, bits):
     """configs[0] shapes plus members of 70 KiB - 1 MiB (several virtual nodes,
     R^e weights) in one batch."""
