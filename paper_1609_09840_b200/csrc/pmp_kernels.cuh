@@ -727,7 +727,16 @@ template <int BITS> struct ChunkOut {
 // the same values.
 // POLY (two-level variant, reading Q19): a2 is a table of 128 field elements
 // (lo, hi pairs) and chunk c is weighted by a2[(c + rot) mod 128].
-template <int BITS, bool POLY = false>
+// LANE (tree only): each lane folds a_{2,c} times its own 3->2-reduced partial
+// of block c (lane r = 0 adds b_1 first) into a per-lane level-2 sum: since
+// a_{2,c} v_1(c) = a_{2,c} (b_1 + sum_lanes P_lane) mod p, the 3 shuffle levels
+// per block are replaced by one 5-level sum per call (v1_first is not set).
+// Per lane and node: 32 (PM+64) / 32 (PM+32) products < 2^(2n+1.6), so the
+// 5- / 3-limb sums hold the whole warp's total.
+#ifndef PMP_L2PF
+#define PMP_L2PF 2   // warp_chunks: bulk L2 prefetch distance in 4 KiB tiles (0: off)
+#endif
+template <int BITS, bool POLY = false, bool LANE = false>
 PMP_DI ChunkOut<BITS> warp_chunks(const StrView &s, uint64_t cb, uint64_t ce, const LaneKeys<BITS> &lk,
                                   uint64_t b1, const uint64_t *__restrict__ a2, int lane, uint32_t rot = 0) {
   using T = Tr<BITS>;
@@ -742,6 +751,19 @@ PMP_DI ChunkOut<BITS> warp_chunks(const StrView &s, uint64_t cb, uint64_t ce, co
   res.v1_first = Fe();
   for (uint64_t c0 = cb; c0 < ce; c0 += CPI) {
     const uint64_t gofs = (c0 + (uint64_t)g * CPG) * (uint64_t)T::CHUNK;  // group block start
+#if PMP_L2PF
+    // bulk L2 prefetch (TMA engine, no registers) of the tile PMP_L2PF ahead,
+    // so that the register-fed loads below find their lines in L2
+    if (lane == 0 && c0 + (uint64_t)PMP_L2PF * CPI < ce) {
+      const uint64_t pf = (c0 + (uint64_t)PMP_L2PF * CPI) * (uint64_t)T::CHUNK;   // global offset
+      const uint64_t pe = min(pf + 4096, s.avail_end);
+      if (pe > pf) {
+        const uintptr_t a = (uintptr_t)(s.base + (pf - s.g0)) & ~(uintptr_t)15;
+        const uint32_t nb = (uint32_t)(((uintptr_t)(s.base + (pe - s.g0)) + 15 - a) & ~(uintptr_t)15);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(nb) : "memory");
+      }
+    }
+#endif
     uint4 U[8];
     load_group_block(s, gofs, lane, U);
     const bool tail = tlast < (c0 + CPI) * 128;  // warp-uniform
@@ -773,6 +795,17 @@ PMP_DI ChunkOut<BITS> warp_chunks(const StrView &s, uint64_t cb, uint64_t ce, co
       part[0] = A[0];
       part[1] = A[1];
     }
+    if constexpr (LANE && !POLY) {
+#pragma unroll
+      for (int cs = 0; cs < CPG; cs++) {
+        const uint64_t c = c0 + (uint64_t)g * CPG + cs;
+        if (c < ce) {
+          Acc x = part[cs];
+          if (r == 0) acc_add_word(x, b1);
+          acc_mac_partial(res.acc2, a2[c & 127], x);
+        }
+      }
+    } else {
     // ---- combine the 8 lanes of each group, reduce, fold into level 2 ----
 #pragma unroll
     for (int cs = 0; cs < CPG; cs++) {
@@ -796,10 +829,11 @@ PMP_DI ChunkOut<BITS> warp_chunks(const StrView &s, uint64_t cb, uint64_t ce, co
         if (c < ce) acc_mac_fe(res.acc2, a2[c & 127], v1);
       }
     }
+    }
   }
-  // sum the four groups' level-2 accumulators
+  // sum the four groups' level-2 accumulators (LANE: all 32 lanes')
 #pragma unroll
-  for (int m = 8; m < 32; m <<= 1) {
+  for (int m = (LANE && !POLY) ? 1 : 8; m < 32; m <<= 1) {
     Acc y = acc_shfl_xor(res.acc2, m);
     acc_add(res.acc2, y);
   }
@@ -1167,50 +1201,67 @@ __device__ __noinline__ void mid_phase(const uint64_t *__restrict__ keys, const 
     produce();                                      // the slot is free: refill it
     // ---- block values (in-group shuffles), level 2
     if (active && t == 0) acc_zero(acc2);
-    uint64_t lo1 = 0;                               // L_eff = 1: V mod 2^n
+    if constexpr (!POLY) {
+      // tree: each lane folds its own 3->2-reduced partial of block c, times
+      // a_{2,c} (weight 1 when the block is the whole tree), into its share of
+      // the string's sum; the group adds the shares when the string ends
 #pragma unroll
-    for (int cs = 0; cs < CPG; cs++) {
-      Acc x = part[cs];
-#pragma unroll
-      for (int m = 1; m < 8; m <<= 1) {
-        Acc y = acc_shfl_xor(x, m);
-        acc_add(x, y);
+      for (int cs = 0; cs < CPG; cs++) {
+        const uint64_t c = (uint64_t)t * CPG + cs;
+        if (active && c < T1) {
+          Acc x = part[cs];
+          if (r == 0) acc_add_word(x, b1);
+          acc_mac_partial(acc2, T1 == 1 ? 1ull : s_a2[c], x);
+        }
       }
-      acc_add_word(x, b1);                          // Eq. (1): b_1 + sum a s
-      const uint64_t c = (uint64_t)t * CPG + cs;
-      if (active && c < T1) {
-        if constexpr (POLY) {                       // W[c + 128 - C] v_1(c)
+      if (__any_sync(FULL, last)) {
+        Acc x = acc2;
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1) {
+          Acc y = acc_shfl_xor(x, m);
+          acc_add(x, y);
+        }
+        if (last) {
+          if (fold) {                               // marker-only block T1 - 1
+            const uint64_t w2[2] = {s_mklo[T1 - 1], s_mkhi[T1 - 1]};
+            Fe m;
+            fe_load(w2, m);
+            acc_add_fe(x, m);
+          }
+          if (T1 > 1) acc_add_word(x, b2);          // b_2
+          if (leader) emit<BITS>(os, si, acc_reduce_lo(x));
+        }
+      }
+    } else {
+      // POLY: block values (in-group shuffles), each fully reduced, weighted W[c + 128 - C]
+#pragma unroll
+      for (int cs = 0; cs < CPG; cs++) {
+        Acc x = part[cs];
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1) {
+          Acc y = acc_shfl_xor(x, m);
+          acc_add(x, y);
+        }
+        acc_add_word(x, b1);                        // Eq. (1): b_1 + sum a s
+        const uint64_t c = (uint64_t)t * CPG + cs;
+        if (active && c < T1) {
           const uint32_t wi = (uint32_t)(c + 128 - T1);
           const uint64_t w2[2] = {s_a2[wi], s_mkhi[wi]};
           Fe w;
           fe_load(w2, w);
           acc_mac_fe_full(acc2, w, acc_reduce(x));
-        } else if (T1 == 1) {
-          lo1 = acc_reduce_lo(x);                   // the whole tree is this block
-        } else {
-          acc_mac_partial(acc2, s_a2[c], x);        // a_{2,c} v_1(c), v_1 3->2-reduced
         }
       }
-    }
-    if (last) {
-      if (fold) {                                   // marker-only block T1 - 1
-        if constexpr (POLY) {
+      if (last) {
+        if (fold) {                                 // marker-only block T1 - 1, at position 127
           const uint64_t w2[2] = {s_a2[127], s_mkhi[127]};
           Fe w;
           fe_load(w2, w);
           acc_mac_fe_full(acc2, w, v1mk);
-        } else {
-          const uint64_t w2[2] = {s_mklo[T1 - 1], s_mkhi[T1 - 1]};
-          Fe m;
-          fe_load(w2, m);
-          acc_add_fe(acc2, m);
         }
+        acc_add_word(acc2, b2);                     // V = b_2 + sum (reading Q19)
+        if (leader) emit<BITS>(os, si, acc_reduce_lo(acc2));
       }
-      if (POLY || T1 > 1) {
-        acc_add_word(acc2, b2);                     // b_2 (POLY: V = b_2 + sum, reading Q19)
-        lo1 = acc_reduce_lo(acc2);
-      }
-      if (leader) emit<BITS>(os, si, lo1);
     }
   }
 }
@@ -1560,9 +1611,25 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     // into the next one (virtual node boundaries fall inside tiles when d > 0)
     const uint64_t qf = (c0 + dsh) >> 7;
     const bool cross = POLY && ((c0 + CPI - 1 + dsh) >> 7) != qf;
+    // tree strings with a level 2: each lane folds a_{2,c} times its own
+    // 3->2-reduced partial (lane r = 0 adds b_1) into its level-2 sum, which
+    // the node close sums over all 32 lanes (see warp_chunks, LANE)
+    const bool lane_sums = !POLY && leff >= 2;
+    if (lane_sums) {
+#pragma unroll
+      for (int cs = 0; cs < CPG; cs++) {
+        const uint64_t c = c0 + (uint64_t)g * CPG + cs;
+        if (c < T1) {
+          Acc x = part[cs];
+          if (r == 0) acc_add_word(x, b1);
+          acc_mac_partial(acc2, s_a2[c & 127], x);
+        }
+      }
+    }
     // ---- combine the 8 lanes of each group, fold into level 2 ----
 #pragma unroll
     for (int cs = 0; cs < CPG; cs++) {
+      if (lane_sums) break;
       Acc x = part[cs];
 #pragma unroll
       for (int m = 1; m < 8; m <<= 1) {
@@ -1632,7 +1699,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     if (leff >= 2 && ((cend & 127) == 0 || cend >= T1)) {
       Acc x = acc2;
 #pragma unroll
-      for (int m = 8; m < 32; m <<= 1) {
+      for (int m = 1; m < 32; m <<= 1) {             // lane sums (!POLY, leff >= 2): all 32 lanes
         Acc y = acc_shfl_xor(x, m);
         acc_add(x, y);
       }
@@ -1718,7 +1785,7 @@ k_node(const uint64_t *__restrict__ keys, StrView s, uint64_t cb, uint64_t ce, u
   lk.load(ak, lane & 7);
   for (uint64_t q = qb + warp; q < qe; q += nw) {
     const uint64_t lo = max(q * 128, cb), hi = min(q * 128 + 128, ce);
-    ChunkOut<BITS> co = warp_chunks<BITS>(s, lo, hi, lk, bk[0], ak + kM, lane);
+    ChunkOut<BITS> co = warp_chunks<BITS, false, true>(s, lo, hi, lk, bk[0], ak + kM, lane);
     const Fe v = acc_reduce(co.acc2);
     if (lane == 0) fe_store(s2 + 2 * (q - qb), v);
   }
@@ -1984,7 +2051,7 @@ k_stream_node(const uint64_t *__restrict__ keys, StrView s, uint64_t c0, uint64_
       const uint64_t lo = max(c, c0), hi = min(c + span, c0 + N);
       Acc x;
       if (lo < hi) {
-        ChunkOut<BITS> co = warp_chunks<BITS>(s, lo, hi, lk, bk[0], ak + kM, lane);
+        ChunkOut<BITS> co = warp_chunks<BITS, false, true>(s, lo, hi, lk, bk[0], ak + kM, lane);
         x = co.acc2;
       } else {
         acc_zero(x);
