@@ -175,6 +175,27 @@ PMP_DI void acc_mac_partial(Acc3 &acc, uint64_t a, const Acc3 &x) {
   reduce3to2_32(x.c0, x.c1, x.c2, v0, v1);
   acc3_mac_v01(acc, (uint32_t)a, v0, v1);
 }
+// the same for a field-element weight w (< p, the extra bit included):
+// w (v0 + v1 2^n) = w_lo (v0 + v1 2^n) + [w >= 2^n] (v0 + v1 2^n) 2^n
+PMP_DI void acc_mac_partial_fe(Acc5 &acc, const Fe64 &w, const Acc5 &x) {
+  uint64_t v0;
+  uint32_t v1;
+  reduce3to2_64(((uint64_t)x.c1 << 32) | x.c0, ((uint64_t)x.c3 << 32) | x.c2, x.c4, v0, v1);
+  acc5_mac_v01(acc, w.lo, v0, v1);
+  if (w.hi) {
+    const Acc5 h = {0, 0, (uint32_t)v0, (uint32_t)(v0 >> 32), v1};
+    acc5_add(acc, h);
+  }
+}
+PMP_DI void acc_mac_partial_fe(Acc3 &acc, uint64_t w, const Acc3 &x) {
+  uint32_t v0, v1;
+  reduce3to2_32(x.c0, x.c1, x.c2, v0, v1);
+  acc3_mac_v01(acc, (uint32_t)w, v0, v1);
+  if (w >> 32) {
+    const Acc3 h = {0, v0, v1};
+    acc3_add(acc, h);
+  }
+}
 // levels of Algorithm 1 applied to T words: 0 if T == 1, else ceil(log_128 T)
 PMP_HDI int levels_of(uint64_t T) {
   return (T > 1) + (T > (1ULL << 7)) + (T > (1ULL << 14)) + (T > (1ULL << 21)) + (T > (1ULL << 28)) +
@@ -727,12 +748,12 @@ template <int BITS> struct ChunkOut {
 // the same values.
 // POLY (two-level variant, reading Q19): a2 is a table of 128 field elements
 // (lo, hi pairs) and chunk c is weighted by a2[(c + rot) mod 128].
-// LANE (tree only): each lane folds a_{2,c} times its own 3->2-reduced partial
+// LANE: each lane folds a_{2,c} times its own 3->2-reduced partial
 // of block c (lane r = 0 adds b_1 first) into a per-lane level-2 sum: since
 // a_{2,c} v_1(c) = a_{2,c} (b_1 + sum_lanes P_lane) mod p, the 3 shuffle levels
 // per block are replaced by one 5-level sum per call (v1_first is not set).
-// Per lane and node: 32 (PM+64) / 32 (PM+32) products < 2^(2n+1.6), so the
-// 5- / 3-limb sums hold the whole warp's total.
+// Per lane and node: 32 products < 2^(2n+1.6) (POLY: weights W < p, products
+// < 2^(2n+2.6)), so the 5- / 3-limb sums hold the whole warp's total.
 #ifndef PMP_L2PF
 #define PMP_L2PF 2   // warp_chunks: bulk L2 prefetch distance in 4 KiB tiles (0: off)
 #endif
@@ -795,14 +816,20 @@ PMP_DI ChunkOut<BITS> warp_chunks(const StrView &s, uint64_t cb, uint64_t ce, co
       part[0] = A[0];
       part[1] = A[1];
     }
-    if constexpr (LANE && !POLY) {
+    if constexpr (LANE) {
 #pragma unroll
       for (int cs = 0; cs < CPG; cs++) {
         const uint64_t c = c0 + (uint64_t)g * CPG + cs;
         if (c < ce) {
           Acc x = part[cs];
           if (r == 0) acc_add_word(x, b1);
-          acc_mac_partial(res.acc2, a2[c & 127], x);
+          if constexpr (POLY) {
+            Fe w;
+            fe_load(a2 + 2 * ((c + rot) & 127), w);
+            acc_mac_partial_fe(res.acc2, w, x);
+          } else {
+            acc_mac_partial(res.acc2, a2[c & 127], x);
+          }
         }
       }
     } else {
@@ -833,7 +860,7 @@ PMP_DI ChunkOut<BITS> warp_chunks(const StrView &s, uint64_t cb, uint64_t ce, co
   }
   // sum the four groups' level-2 accumulators (LANE: all 32 lanes')
 #pragma unroll
-  for (int m = (LANE && !POLY) ? 1 : 8; m < 32; m <<= 1) {
+  for (int m = LANE ? 1 : 8; m < 32; m <<= 1) {
     Acc y = acc_shfl_xor(res.acc2, m);
     acc_add(res.acc2, y);
   }
@@ -1201,66 +1228,50 @@ __device__ __noinline__ void mid_phase(const uint64_t *__restrict__ keys, const 
     produce();                                      // the slot is free: refill it
     // ---- block values (in-group shuffles), level 2
     if (active && t == 0) acc_zero(acc2);
-    if constexpr (!POLY) {
-      // tree: each lane folds its own 3->2-reduced partial of block c, times
-      // a_{2,c} (weight 1 when the block is the whole tree), into its share of
-      // the string's sum; the group adds the shares when the string ends
+    // each lane folds its own 3->2-reduced partial of block c, times the
+    // block's level-2 weight (tree: a_{2,c}, or 1 when the block is the whole
+    // tree; POLY: W[c + 128 - C]), into its share of the string's sum; the
+    // group adds the shares when the string ends
 #pragma unroll
-      for (int cs = 0; cs < CPG; cs++) {
-        const uint64_t c = (uint64_t)t * CPG + cs;
-        if (active && c < T1) {
-          Acc x = part[cs];
-          if (r == 0) acc_add_word(x, b1);
+    for (int cs = 0; cs < CPG; cs++) {
+      const uint64_t c = (uint64_t)t * CPG + cs;
+      if (active && c < T1) {
+        Acc x = part[cs];
+        if (r == 0) acc_add_word(x, b1);
+        if constexpr (POLY) {
+          const uint32_t wi = (uint32_t)(c + 128 - T1);
+          const uint64_t w2[2] = {s_a2[wi], s_mkhi[wi]};
+          Fe w;
+          fe_load(w2, w);
+          acc_mac_partial_fe(acc2, w, x);
+        } else {
           acc_mac_partial(acc2, T1 == 1 ? 1ull : s_a2[c], x);
         }
       }
-      if (__any_sync(FULL, last)) {
-        Acc x = acc2;
+    }
+    if (__any_sync(FULL, last)) {
+      Acc x = acc2;
 #pragma unroll
-        for (int m = 1; m < 8; m <<= 1) {
-          Acc y = acc_shfl_xor(x, m);
-          acc_add(x, y);
-        }
-        if (last) {
-          if (fold) {                               // marker-only block T1 - 1
+      for (int m = 1; m < 8; m <<= 1) {
+        Acc y = acc_shfl_xor(x, m);
+        acc_add(x, y);
+      }
+      if (last) {
+        if (fold) {                                 // marker-only block T1 - 1
+          if constexpr (POLY) {                     // at position 127: W[127] v_1
+            const uint64_t w2[2] = {s_a2[127], s_mkhi[127]};
+            Fe w;
+            fe_load(w2, w);
+            acc_mac_fe_full(x, w, v1mk);
+          } else {
             const uint64_t w2[2] = {s_mklo[T1 - 1], s_mkhi[T1 - 1]};
             Fe m;
             fe_load(w2, m);
             acc_add_fe(x, m);
           }
-          if (T1 > 1) acc_add_word(x, b2);          // b_2
-          if (leader) emit<BITS>(os, si, acc_reduce_lo(x));
         }
-      }
-    } else {
-      // POLY: block values (in-group shuffles), each fully reduced, weighted W[c + 128 - C]
-#pragma unroll
-      for (int cs = 0; cs < CPG; cs++) {
-        Acc x = part[cs];
-#pragma unroll
-        for (int m = 1; m < 8; m <<= 1) {
-          Acc y = acc_shfl_xor(x, m);
-          acc_add(x, y);
-        }
-        acc_add_word(x, b1);                        // Eq. (1): b_1 + sum a s
-        const uint64_t c = (uint64_t)t * CPG + cs;
-        if (active && c < T1) {
-          const uint32_t wi = (uint32_t)(c + 128 - T1);
-          const uint64_t w2[2] = {s_a2[wi], s_mkhi[wi]};
-          Fe w;
-          fe_load(w2, w);
-          acc_mac_fe_full(acc2, w, acc_reduce(x));
-        }
-      }
-      if (last) {
-        if (fold) {                                 // marker-only block T1 - 1, at position 127
-          const uint64_t w2[2] = {s_a2[127], s_mkhi[127]};
-          Fe w;
-          fe_load(w2, w);
-          acc_mac_fe_full(acc2, w, v1mk);
-        }
-        acc_add_word(acc2, b2);                     // V = b_2 + sum (reading Q19)
-        if (leader) emit<BITS>(os, si, acc_reduce_lo(acc2));
+        if (POLY || T1 > 1) acc_add_word(x, b2);    // b_2 (POLY: V = b_2 + sum, reading Q19)
+        if (leader) emit<BITS>(os, si, acc_reduce_lo(x));
       }
     }
   }
@@ -1614,7 +1625,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     // tree strings with a level 2: each lane folds a_{2,c} times its own
     // 3->2-reduced partial (lane r = 0 adds b_1) into its level-2 sum, which
     // the node close sums over all 32 lanes (see warp_chunks, LANE)
-    const bool lane_sums = !POLY && leff >= 2;
+    const bool lane_sums = POLY || leff >= 2;
     if (lane_sums) {
 #pragma unroll
       for (int cs = 0; cs < CPG; cs++) {
@@ -1622,7 +1633,16 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
         if (c < T1) {
           Acc x = part[cs];
           if (r == 0) acc_add_word(x, b1);
-          acc_mac_partial(acc2, s_a2[c & 127], x);
+          if constexpr (POLY) {                     // W[(c + d) mod 128] times the lane's share
+            const uint32_t wi = (uint32_t)(c + dsh) & 127;
+            const uint64_t w2[2] = {s_a2[wi], s_mkhi[wi]};
+            Fe w;
+            fe_load(w2, w);
+            if (cross && ((c + dsh) >> 7) != qf) acc_mac_partial_fe(acc2b, w, x);
+            else acc_mac_partial_fe(acc2, w, x);
+          } else {
+            acc_mac_partial(acc2, s_a2[c & 127], x);
+          }
         }
       }
     }
@@ -1680,7 +1700,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
       for (uint64_t qn = qf; qn < Qp && cv >= 128 * (qn + 1); qn++) {
         Acc x = acc2;
 #pragma unroll
-        for (int m = 8; m < 32; m <<= 1) {
+        for (int m = 1; m < 32; m <<= 1) {            // lane sums: all 32 lanes
           Acc y = acc_shfl_xor(x, m);
           acc_add(x, y);
         }

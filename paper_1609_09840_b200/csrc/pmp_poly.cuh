@@ -58,7 +58,7 @@ PMP_DI typename Tr<BITS>::Acc poly_nodes(const uint64_t *__restrict__ keys, cons
     const uint64_t first = q * 128 >= d ? q * 128 - d : 0;
     const uint64_t lo = max(first, cb), hi = min(q * 128 + 128 - d, ce);
     if (lo >= hi) continue;
-    ChunkOut<BITS> co = warp_chunks<BITS, true>(s, lo, hi, lk, keys[0], keys + kPolyW, lane, d);
+    ChunkOut<BITS> co = warp_chunks<BITS, true, true>(s, lo, hi, lk, keys[0], keys + kPolyW, lane, d);
     Fe nv = acc_reduce(co.acc2);
     if (q + 1 < Qp) nv = fe_mul(nv, poly_pow_R<BITS>(keys, Qp - 1 - q));  // same value in every lane
     acc_add_fe(sum, nv);
