@@ -248,6 +248,8 @@ def main():
     ap.add_argument("--variant", default="tree", choices=["tree", "two-level"],
                     help="two-level: the multilinear + polynomial variant (8(f4), pmp_hash2_*)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--separate-widths", action="store_true",
+                    help="hash the two widths of configs[1] with two pmp_hash_batch calls instead of one fused pass")
     ap.add_argument("--e2e-piece-mib", type=int, default=64, help="piece size of the host-resident e2e path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -347,7 +349,14 @@ def main():
 
         counts = torch.zeros(max(args.buckets, 1), dtype=torch.int32, device=dev)
 
+        fused = len(wl.bits) == 2 and not v2 and not args.buckets and not args.separate_widths
+
         def step():
+            if fused:  # both outputs of the batch in one pass over the short strings (pmp_hash_batch_multi)
+                pmp._check(pmp.pmp_hash_batch_multi([keys[b].handle for b in wl.bits], d_pay.data_ptr(),
+                                                    d_off.data_ptr(), n, [outs[b].data_ptr() for b in wl.bits], sp),
+                           "pmp_hash_batch_multi")
+                return
             for b in wl.bits:
                 if args.buckets:
                     pmp._check(pmp.pmp_hash_batch_buckets(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
@@ -358,8 +367,12 @@ def main():
                     pmp._check(fn(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
                                   outs[b].data_ptr(), sp), "pmp_hash_batch")
         dominant = "k_short" if wl.hi <= 127 else "k_wstring"
-        # algorithmic bytes per dominant launch: payload + offsets + digests (avg over widths)
-        alg_bytes_per_launch = total_bytes + 8 * (n + 1) + n * sum(b // 8 for b in wl.bits) / len(wl.bits)
+        # algorithmic bytes per dominant launch: payload + offsets + digests (fused: both
+        # widths' digests in one launch; otherwise the average over the widths' launches)
+        if fused and dominant == "k_short":
+            alg_bytes_per_launch = total_bytes + 8 * (n + 1) + n * sum(b // 8 for b in wl.bits)
+        else:
+            alg_bytes_per_launch = total_bytes + 8 * (n + 1) + n * sum(b // 8 for b in wl.bits) / len(wl.bits)
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):

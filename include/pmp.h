@@ -121,6 +121,16 @@ int pmp_hash_batch_buckets(const pmp_keys *keys, const uint8_t *bytes, const uin
                            uint64_t n, uint32_t M, uint32_t *buckets, uint32_t *counts,
                            struct CUstream_st *stream);
 
+#define PMP_HOST_MAX_KEYS 4
+/* Several key schedules over one device batch (1 <= nkeys <= PMP_HOST_MAX_KEYS;
+ * outs[k]: device, n digests for keys[k]).  Equal to nkeys pmp_hash_batch
+ * calls; a 64-bit and a 32-bit schedule are paired into one fused pass over
+ * the short strings (each string read once for both digests, configs[1]'s
+ * "both 32-bit and 64-bit outputs"), long strings are hashed per schedule.
+ * Errors as pmp_hash_batch. */
+int pmp_hash_batch_multi(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
+                         uint64_t n, void *const *outs, struct CUstream_st *stream);
+
 /* Host-resident batch (the e2e path): the same digests as pmp_hash_batch for
  * bytes / offsets / outs in HOST memory, under nkeys key schedules at once
  * (1 <= nkeys <= PMP_HOST_MAX_KEYS; e.g. a 64-bit and a 32-bit schedule, all on
@@ -138,7 +148,6 @@ int pmp_hash_batch_buckets(const pmp_keys *keys, const uint8_t *bytes, const uin
  * point (synchronise it before reading outs); the host buffers must stay
  * valid until then.  Device scratch is stream-ordered and released by then.
  * Errors as pmp_hash_batch, and PMP_EINVAL for keys on different devices. */
-#define PMP_HOST_MAX_KEYS 4
 int pmp_hash_batch_host(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
                         uint64_t n, void *const *outs, uint64_t piece_bytes, struct CUstream_st *stream);
 

@@ -52,6 +52,7 @@ def lib() -> ctypes.CDLL:
             "pmp_hash_batch": ([_vp, _vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_batch_buckets": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _vp, _vp], _int),
             "pmp_hash_batch_host": ([_vp, _int, _vp, _vp, _u64, _vp, _u64, _vp], _int),
+            "pmp_hash_batch_multi": ([_vp, _int, _vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_long": ([_vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_long_partial": ([_vp, _vp, _u64, _u64, _u64, _vp, _vp], _int),
             "pmp_hash_long_combine": ([_vp, _vp, _int, _u64, _vp, _vp], _int),
@@ -124,6 +125,13 @@ def pmp_keys_free(keys: int) -> None:
 
 def pmp_hash_batch(keys: int, bytes_ptr: int, offsets_ptr: int, n: int, out_ptr: int, stream: int) -> int:
     return lib().pmp_hash_batch(keys, bytes_ptr, offsets_ptr, n, out_ptr, stream)
+
+
+def pmp_hash_batch_multi(keys: list, bytes_ptr: int, offsets_ptr: int, n: int, out_ptrs: list, stream: int) -> int:
+    """keys: list of pmp_keys* handles; out_ptrs: one device digest buffer per key."""
+    ka = (_vp * len(keys))(*keys)
+    oa = (_vp * len(out_ptrs))(*out_ptrs)
+    return lib().pmp_hash_batch_multi(ka, len(keys), bytes_ptr, offsets_ptr, n, oa, stream)
 
 
 def pmp_hash_batch_host(keys: list, bytes_ptr: int, offsets_ptr: int, n: int, out_ptrs: list,
@@ -299,6 +307,20 @@ def hash_batch(keys: Keys, payload, offsets, out=None, stream=None):
     _check(pmp_hash_batch(keys.handle, payload.data_ptr(), offsets.data_ptr(), max(n, 0),
                           out.data_ptr(), _stream_ptr(stream)), "pmp_hash_batch")
     return out
+
+
+def hash_batch_multi(keys: list, payload, offsets, outs=None, stream=None):
+    """Several key schedules over one device batch (a 64-bit + 32-bit pair is
+    fused into one pass over the short strings); returns one digest tensor per key."""
+    import torch
+
+    n = offsets.numel() - 1
+    if outs is None:
+        outs = [torch.empty(max(n, 0), dtype=torch.int64 if k.bits == 64 else torch.int32, device=offsets.device)
+                for k in keys]
+    _check(pmp_hash_batch_multi([k.handle for k in keys], payload.data_ptr(), offsets.data_ptr(), max(n, 0),
+                                [o.data_ptr() for o in outs], _stream_ptr(stream)), "pmp_hash_batch_multi")
+    return outs
 
 
 def hash_batch_host(keys: list, payload, offsets, outs=None, piece_bytes: int = 0):

@@ -639,28 +639,59 @@ void pmp_keys_free(pmp_keys *k) {
   delete k;
 }
 
+// Resident blocks per SM of a kernel (registers, shared memory), cached: the
+// persistent grids are exactly one wave.
+static int resident_blocks(const void *f, int threads, size_t smem, const char *name) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void *, int>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &e : cache)
+    if (e.first == f) return e.second;
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, threads, smem);
+  if (b < 1) b = 1;
+  if (getenv("PMP_VERBOSE")) fprintf(stderr, "pmp: %s smem %zu B, %d blocks/SM\n", name, smem, b);
+  cache.push_back({f, b});
+  return b;
+}
+
+// One batch under schedule k (digests to os) and, for the dual-width fused
+// short-string pass, a second schedule k2 (k 64-bit, k2 32-bit, tree only;
+// digests to *os2): short strings are read once for both, long strings (the
+// work list, shared) are hashed per schedule by k_wstring.
 static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
-                           const OutSpec &os, cudaStream_t st, bool v2 = false) {
+                           const OutSpec &os, cudaStream_t st, bool v2 = false, const pmp_keys *k2 = nullptr,
+                           const OutSpec *os2 = nullptr) {
   if (!k) return PMP_EINVAL;
   if (n == 0) return 0;
   if (!bytes || !offsets || !os.out || n >= (1ULL << 32)) return PMP_EINVAL;
   if (int rc = check_keys(k)) return rc;
+  const bool dual = k2 != nullptr;
+  if (dual && (!os2 || !os2->out || v2 || k->bits != 64 || k2->bits != 32 || k2->device != k->device))
+    return PMP_EINVAL;
   const int sms = sm_count(k->device);
   Scratch sc(st), sc_off(st);
-  // work list (n u32) + counters [mid, big, next]
+  // work list (n u32) + counters [mid, big, next big, next mid batch]
   if (sc.alloc((size_t)n * 4 + 16)) return PMP_ENOMEM;
   uint32_t *wcount = (uint32_t *)sc.p;
   uint32_t *wlist = wcount + 4;
   if (cudaMemsetAsync(wcount, 0, 16, st) != cudaSuccess) return PMP_ECUDA;
-  const ParamKeys pk = param_keys(k);
+  ParamKeys pk = param_keys(k);
+  if (dual) {
+    for (int i = 0; i < 32; i++) pk.a32[i] = (uint32_t)k2->a[i];
+    pk.b32 = k2->b[0];
+  }
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    const void *fs[4] = {(const void *)k_short<64>, (const void *)k_short<32>, (const void *)k_short<64, true>,
-                         (const void *)k_short<32, true>};
+    const void *fs[5] = {(const void *)k_short<64>, (const void *)k_short<32>, (const void *)k_short<64, true>,
+                         (const void *)k_short<32, true>, (const void *)k_short<64, false, true>};
     for (const void *f : fs) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     }
+    const void *ws[4] = {(const void *)k_wstring<64>, (const void *)k_wstring<32>, (const void *)k_wstring<64, true>,
+                         (const void *)k_wstring<32, true>};
+    for (const void *f : ws) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
   });
   // the offsets ring is fed by TMA bulk copies, which need 16-byte aligned sources
   if ((uintptr_t)offsets & 15) {
@@ -671,74 +702,39 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     sc_off.p = al;
     offsets = (const uint64_t *)al;
   }
-  uint64_t grid = (n + kTile - 1) / kTile;
+  // ---- short strings (and the work list of long ones)
+  const void *kshort = dual ? (const void *)k_short<64, false, true>
+                            : v2 ? (k->bits == 64 ? (const void *)k_short<64, true> : (const void *)k_short<32, true>)
+                                 : (k->bits == 64 ? (const void *)k_short<64> : (const void *)k_short<32>);
   const int threads = (kShortWarps + 1) * 32;  // + producer warp
-  static int sper_sm[2][2] = {{0, 0}, {0, 0}};   // resident blocks per SM [v2][64-bit]
-  int &sps = sper_sm[v2][k->bits == 64];
-  if (sps == 0) {
-    if (v2)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sps, k->bits == 64 ? (const void *)k_short<64, true> : (const void *)k_short<32, true>, threads, kShortSmem);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sps, k->bits == 64 ? (const void *)k_short<64> : (const void *)k_short<32>, threads, kShortSmem);
-    if (sps < 1) sps = 1;
-    if (getenv("PMP_VERBOSE")) fprintf(stderr, "pmp: k_short smem %zu B, %d blocks/SM\n", kShortSmem, sps);
-  }
-  const uint64_t maxgrid = (uint64_t)sms * sps;  // persistent grid
+  uint64_t grid = (n + kTile - 1) / kTile;
+  const uint64_t maxgrid = (uint64_t)sms * resident_blocks(kshort, threads, kShortSmem, "k_short");  // persistent grid
   if (grid > maxgrid) grid = maxgrid;
-  int rc;
-  if (v2) {  // two-level variant (8(f4)): short strings in k_short, the rest warp per string
-    if (k->bits == 64)
-      rc = launch("k_short", st, [&] { k_short<64, true><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
-    else
-      rc = launch("k_short", st, [&] { k_short<32, true><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
-    if (rc) return rc;
-    static std::once_flag pattr_once;
-    std::call_once(pattr_once, [] {
-      cudaFuncSetAttribute(k_wstring<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
-      cudaFuncSetAttribute(k_wstring<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
-    });
-    static int pper_sm[2] = {0, 0};
-    int &pps = pper_sm[k->bits == 64];
-    if (pps == 0) {
-      if (k->bits == 64)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pps, k_wstring<64, true>, kWBlockWarps * 32, kWSmem);
-      else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pps, k_wstring<32, true>, kWBlockWarps * 32, kWSmem);
-      if (pps < 1) pps = 1;
-    }
-    const unsigned pgrid = (unsigned)(sms * pps);
-    if (k->bits == 64)
-      return launch("k_wstring", st, [&] { k_wstring<64, true><<<pgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
-    return launch("k_wstring", st, [&] { k_wstring<32, true><<<pgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
-  }
-  if (k->bits == 64)
-    rc = launch("k_short", st, [&] { k_short<64><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
-  else
-    rc = launch("k_short", st, [&] { k_short<32><<<(unsigned)grid, threads, kShortSmem, st>>>(pk, bytes, offsets, n, os, wlist, wcount); });
-  if (rc) return rc;
-  static std::once_flag wattr_once;
-  std::call_once(wattr_once, [] {
-    cudaFuncSetAttribute(k_wstring<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
-    cudaFuncSetAttribute(k_wstring<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+  const OutSpec o2 = dual ? *os2 : os;
+  int rc = launch("k_short", st, [&] {
+    void *args[] = {(void *)&pk, (void *)&bytes, (void *)&offsets, (void *)&n, (void *)&os, (void *)&wlist,
+                    (void *)&wcount, (void *)&o2};
+    cudaLaunchKernel(kshort, dim3((unsigned)grid), dim3(threads), args, kShortSmem, st);
   });
-  // persistent grid: exactly the resident blocks (registers and shared memory),
-  // since mid strings are strided statically over the warps
-  static int wper_sm[2] = {0, 0};
-  int &wps = wper_sm[k->bits == 64];
-  if (wps == 0) {
-    if (k->bits == 64)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wps, k_wstring<64>, kWBlockWarps * 32, kWSmem);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wps, k_wstring<32>, kWBlockWarps * 32, kWSmem);
-    if (wps < 1) wps = 1;
-    if (getenv("PMP_VERBOSE")) fprintf(stderr, "pmp: k_wstring smem %zu B, %d blocks/SM\n", kWSmem, wps);
-  }
-  const unsigned wgrid = (unsigned)(sms * wps);
-  if (k->bits == 64)
-    rc = launch("k_wstring", st, [&] { k_wstring<64><<<wgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
-  else
-    rc = launch("k_wstring", st, [&] { k_wstring<32><<<wgrid, kWBlockWarps * 32, kWSmem, st>>>(k->d_blob, bytes, offsets, n, os, wlist, wcount); });
-  return rc;
+  if (rc) return rc;
+  // ---- long strings: warp per big string, 8-lane group per mid string (persistent
+  // grid of exactly the resident blocks)
+  auto launch_w = [&](const pmp_keys *kk, const OutSpec &o) -> int {
+    const void *kw = v2 ? (kk->bits == 64 ? (const void *)k_wstring<64, true> : (const void *)k_wstring<32, true>)
+                        : (kk->bits == 64 ? (const void *)k_wstring<64> : (const void *)k_wstring<32>);
+    const unsigned wgrid = (unsigned)(sms * resident_blocks(kw, kWBlockWarps * 32, kWSmem, "k_wstring"));
+    const uint64_t *blob = kk->d_blob;
+    return launch("k_wstring", st, [&] {
+      void *args[] = {(void *)&blob, (void *)&bytes, (void *)&offsets, (void *)&n, (void *)&o, (void *)&wlist,
+                      (void *)&wcount};
+      cudaLaunchKernel(kw, dim3(wgrid), dim3(kWBlockWarps * 32), args, kWSmem, st);
+    });
+  };
+  rc = launch_w(k, os);
+  if (rc || !dual) return rc;
+  // second schedule over the same work list: reset the claim counters
+  if (cudaMemsetAsync(wcount + 2, 0, 8, st) != cudaSuccess) return PMP_ECUDA;
+  return launch_w(k2, *os2);
 }
 
 int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
@@ -758,6 +754,30 @@ int pmp_hash_batch_buckets(const pmp_keys *k, const uint8_t *bytes, const uint64
   os.M = M;
   os.counts = counts;
   return hash_batch_impl(k, bytes, offsets, n, os, st);
+}
+
+int pmp_hash_batch_multi(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
+                         uint64_t n, void *const *outs, cudaStream_t st) {
+  if (!keys || !outs || nkeys < 1 || nkeys > PMP_HOST_MAX_KEYS) return PMP_EINVAL;
+  for (int k = 0; k < nkeys; k++)
+    if (!keys[k] || !outs[k]) return PMP_EINVAL;
+  bool done[PMP_HOST_MAX_KEYS] = {false, false, false, false};
+  // pair a 64-bit with a 32-bit schedule: one fused pass over the short strings
+  for (int k = 0; k < nkeys; k++) {
+    if (done[k] || keys[k]->bits != 64) continue;
+    for (int j = 0; j < nkeys; j++) {
+      if (done[j] || keys[j]->bits != 32 || keys[j]->device != keys[k]->device) continue;
+      OutSpec a{outs[k], 0, nullptr}, b{outs[j], 0, nullptr};
+      if (int rc = hash_batch_impl(keys[k], bytes, offsets, n, a, st, false, keys[j], &b)) return rc;
+      done[k] = done[j] = true;
+      break;
+    }
+  }
+  for (int k = 0; k < nkeys; k++) {
+    if (done[k]) continue;
+    if (int rc = pmp_hash_batch(keys[k], bytes, offsets, n, outs[k], st)) return rc;
+  }
+  return 0;
 }
 
 // Host-resident batches: string-aligned pieces streamed through the device on
@@ -833,12 +853,13 @@ int pmp_hash_batch_host(const pmp_keys *const *keys, int nkeys, const uint8_t *b
     if (nb && cudaMemcpyAsync(d_b + sh, bytes + b0, nb, cudaMemcpyHostToDevice, st[q]) != cudaSuccess) rc = PMP_ECUDA;
     if (!rc && cudaMemcpyAsync(d_o, offsets + s0, (cnt + 1) * 8, cudaMemcpyHostToDevice, st[q]) != cudaSuccess)
       rc = PMP_ECUDA;
+    void *d_outs[PMP_HOST_MAX_KEYS];
+    for (int k = 0; k < nkeys; k++) d_outs[k] = d_d + (size_t)k * ((cap_d + 255) & ~(size_t)255);
+    if (!rc) rc = pmp_hash_batch_multi(keys, nkeys, d_base, d_o, cnt, d_outs, st[q]);
     for (int k = 0; k < nkeys && !rc; k++) {
       const size_t w = keys[k]->bits / 8;
-      uint8_t *d_out = d_d + (size_t)k * ((cap_d + 255) & ~(size_t)255);
-      rc = pmp_hash_batch(keys[k], d_base, d_o, cnt, d_out, st[q]);
-      if (!rc && cudaMemcpyAsync((uint8_t *)outs[k] + s0 * w, d_out, cnt * w, cudaMemcpyDeviceToHost, st[q]) !=
-                     cudaSuccess)
+      if (cudaMemcpyAsync((uint8_t *)outs[k] + s0 * w, d_outs[k], cnt * w, cudaMemcpyDeviceToHost, st[q]) !=
+          cudaSuccess)
         rc = PMP_ECUDA;
     }
   }

@@ -47,6 +47,9 @@ struct ParamKeys {
   uint64_t a[32];
   uint64_t b;
   uint64_t r, b2;  // two-level variant (reading Q19): r = a_{2,1}, b_2
+  // dual-width k_short: the 32-bit schedule's a_{1,0..31} and b_1 (a, b hold the 64-bit one)
+  uint32_t a32[32];
+  uint64_t b32;
 };
 
 // ------------------------------------------------------------- helpers
@@ -315,6 +318,61 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
   }
 }
 
+// Both digests of one short string in one pass (a 64-bit and a 32-bit key
+// schedule: the two configs[1] outputs).  The 32-bit words of PM+32 are the
+// halves of the 64-bit words of PM+64, so the loads, funnel shifts and the
+// loop are shared; each width keeps its own marker word, masks, exact sum and
+// reduction.  The loop covers the 64-bit words holding full 32-bit words,
+// (tf32 + 1) / 2 >= tlast64 of them, warp maximum tfull_max.
+template <class Fetch>
+PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ skeys, const uint32_t *__restrict__ skeys32,
+                            uint32_t B, uint32_t sh, int tfull_max, Fetch fetch, uint64_t &lo64, uint32_t &lo32) {
+  const int tl64 = (int)(B >> 3), tl32 = (int)(B >> 2);
+  MacAcc64 A;
+  macc_zero(A);
+  Acc3 C = {0, 0, 0};
+  uint32_t y0 = fetch(0);
+#pragma unroll
+  for (int tb = 0; tb < 16; tb += kShortG64) {
+    if (tb >= tfull_max) break;                              // warp-uniform
+#pragma unroll
+    for (int j = 0; j < kShortG64; j++) {
+      const int t = tb + j;
+      if (t >= 16) break;                                    // compile-time
+      const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
+      const uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
+      y0 = y2;
+      const bool f64 = t < tl64;
+      if (t < 15) mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), f64 ? lo : 0u, f64 ? hi : 0u);  // Eq. (1)
+      mac32(C, K.a32[2 * t], 2 * t < tl32 ? lo : 0u);
+      if (t < 15) mac32(C, K.a32[2 * t + 1], 2 * t + 1 < tl32 ? hi : 0u);
+    }
+  }
+  // marker words: the 8 bytes at 8 tl64, and its half holding byte 4 tl32
+  const uint32_t z0 = fetch(2 * tl64), z1 = fetch(2 * tl64 + 1), z2 = fetch(2 * tl64 + 2);
+  const uint32_t zl = funnel(z0, z1, sh), zh = funnel(z1, z2, sh);
+  const uint32_t r64 = B & 7, r32 = B & 3;
+  uint64_t w = ((uint64_t)zh << 32) | zl;
+  w = (w & ((1ULL << (8 * r64)) - 1)) | (1ULL << (8 * r64));
+  uint32_t w32 = r64 < 4 ? zl : zh;
+  w32 = (w32 & ((1u << (8 * r32)) - 1)) | (1u << (8 * r32));
+  if (tl64 == 0) {
+    lo64 = w;                                                // |sigma| = 1 (reading Q2)
+  } else {
+    mac64(A, skeys[tl64], w);
+    Acc5 x = macc_normalize(A);
+    acc5_add_u64(x, K.b);
+    lo64 = reduce_lo_acc5(x);
+  }
+  if (tl32 == 0) {
+    lo32 = w32;
+  } else {
+    mac32(C, skeys32[tl32], w32);
+    acc3_add_u64(C, K.b32);
+    lo32 = reduce_lo_acc3(C);
+  }
+}
+
 // ---- TMA bulk-copy / mbarrier helpers (cp.async.bulk -> UBLKCP in SASS)
 PMP_DI uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 PMP_DI void mbar_init(uint64_t *bar, uint32_t count) {
@@ -419,24 +477,28 @@ struct TileHdr {
   uint32_t pos;    // ring position of staged byte 0
   uint32_t mode;   // 0 staged, 1 direct
 };
-constexpr size_t kShortSmem = 256 /* keys */ + kByteRing + kSlack + 16 + (size_t)kRing * kOffBytes +
+constexpr size_t kShortSmem = 384 /* keys */ + kByteRing + kSlack + 16 + (size_t)kRing * kOffBytes +
                               (size_t)kRing * sizeof(TileHdr) +
                               (size_t)(3 * kRing) * 8 + (PMP_SHORT_SORT ? 256 /* sort histograms */ + 2 * kTile /* permutation */ : 0) + 128;
 
-template <int BITS, bool V2 = false>
+// DUAL: BITS = 64 and a second, 32-bit schedule in K.a32 / K.b32 whose digests go to os2
+template <int BITS, bool V2 = false, bool DUAL = false>
 __global__ void __launch_bounds__((kShortWarps + 1) * 32)
 k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets,
-        uint64_t n, const OutSpec os, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
+        uint64_t n, const OutSpec os, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount,
+        const OutSpec os2) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint64_t *skeys = reinterpret_cast<uint64_t *>(smem);                       // a_{1,0..31}
-  uint8_t *ring = smem + 256;                                                  // kByteRing (+ slack)
+  uint32_t *skeys32 = reinterpret_cast<uint32_t *>(smem + 256);               // DUAL: 32-bit a_{1,0..31}
+  uint8_t *ring = smem + 384;                                                  // kByteRing (+ slack)
   uint64_t *offs = reinterpret_cast<uint64_t *>(ring + kByteRing + kSlack + 16);  // kRing x kOffBytes
   TileHdr *hdr = reinterpret_cast<TileHdr *>(reinterpret_cast<uint8_t *>(offs) + (size_t)kRing * kOffBytes);
   uint64_t *bar_off = reinterpret_cast<uint64_t *>(hdr + kRing);  // offsets landed (producer)
   uint64_t *bar_done = bar_off + kRing;                            // tile consumed (producer)
   uint64_t *bar_full = bar_done + kRing;                           // tile ready (consumers)
   if (threadIdx.x < 32) skeys[threadIdx.x] = K.a[threadIdx.x];
+  if (DUAL && threadIdx.x < 32) skeys32[threadIdx.x] = K.a32[threadIdx.x];
 #if PMP_SHORT_SORT
   uint32_t *s_hist = reinterpret_cast<uint32_t *>(bar_full + kRing);  // 2 x 32 class counters
   uint16_t *s_perm = reinterpret_cast<uint16_t *>(s_hist + 64);      // kTile sorted slots
@@ -601,25 +663,34 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     }
 #endif
     // warp max of the number of full words (the marker word is handled apart)
-    const int tfm = (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
+    const int tfm = DUAL ? (int)__reduce_max_sync(FULL, is_short ? ((B >> 2) + 1) >> 1 : 0u)
+                         : (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
     if (is_short) {
       uint64_t lo;
+      uint32_t lo32 = 0;
       if (mode == 0) {
         // (lanes past n read the tile's first bytes: in bounds, result not stored)
         const uint32_t sofs = rpos + (valid ? (uint32_t)((uintptr_t)(bytes + o0) - (uintptr_t)ralo) : 0u);
         const uint32_t pa = ring_s + (sofs & ~3u);
-        lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (sofs & 3), tfm, [&](int kk) { return lds_u32(pa + 4 * kk); });
+        auto fetch = [&](int kk) { return lds_u32(pa + 4 * kk); };
+        if constexpr (DUAL) short_tree_dual(K, skeys, skeys32, B, 8 * (sofs & 3), tfm, fetch, lo, lo32);
+        else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (sofs & 3), tfm, fetch);
       } else {
         // direct tile: read the string's aligned 32-bit words straight from global,
         // touching only words that overlap [start, end) (never past offsets[n]).
         const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
         const uintptr_t pa = sa & ~(uintptr_t)3;
-        lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, [&](int kk) {
+        auto fetch = [&](int kk) {
           const uintptr_t a = pa + 4 * (uintptr_t)kk;
           return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
-        });
+        };
+        if constexpr (DUAL) short_tree_dual(K, skeys, skeys32, B, 8 * (uint32_t)(sa & 3), tfm, fetch, lo, lo32);
+        else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, fetch);
       }
-      if (valid) emit<BITS>(os, i, lo);
+      if (valid) {
+        emit<BITS>(os, i, lo);
+        if constexpr (DUAL) emit<32>(os2, i, lo32);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive_s(done_s + 8 * q);

@@ -434,3 +434,31 @@ def test_host_batch_streaming(torch_dev, oracle_lib, piece):
     assert np.array_equal(got64, oracle_batch(oracle_lib, 41, 64, pay, off))
     assert np.array_equal(got32, oracle_batch(oracle_lib, 42, 32, pay, off))
     assert np.array_equal(got64, run_batch(torch_dev, k64, pay, off))
+
+
+@pytest.mark.parametrize("order", [(64, 32), (32, 64), (64, 64, 32), (32,)])
+def test_multi_schedule_fused_pass(torch_dev, oracle_lib, order):
+    """pmp_hash_batch_multi: a 64-bit and a 32-bit schedule are fused into one
+    pass over the short strings (the 32-bit words are the halves of the 64-bit
+    ones; markers and masks per width), long strings per schedule over the
+    shared work list.  Every length 0..300 (both markers in every position,
+    both |sigma| = 1 cases), all alignments, plus long members; equal to the
+    oracle under each schedule."""
+    import torch
+
+    rng = np.random.default_rng(len(order))
+    lens = np.concatenate([np.repeat(np.arange(0, 301), 3), [5000, 70_000, 1024, 4096, 0]]).astype(np.uint64)
+    rng.shuffle(lens)
+    off = datagen.offsets_from_lengths(lens) + 9
+    pay = datagen.payload_host(51, 0, int(off[-1]))
+    seeds = [51 + i for i in range(len(order))]
+    keys = [pmp.Keys.generate(s, b) for s, b in zip(seeds, order)]
+    d_pay = torch.from_numpy(pay).to(torch_dev)
+    d_off = torch.from_numpy(off.view(np.int64)).to(torch_dev)
+    outs = pmp.hash_batch_multi(keys, d_pay, d_off)
+    torch.cuda.synchronize()
+    for s, b, o in zip(seeds, order, outs):
+        got = pmp.as_u64(o)
+        want = oracle_batch(oracle_lib, s, b, pay, off)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (b, [(int(i), int(lens[i])) for i in bad[:8]])
