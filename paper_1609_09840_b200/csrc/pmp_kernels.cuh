@@ -342,20 +342,23 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
       const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
       const uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
       y0 = y2;
+      // 2t+1 < tl32 <=> t < tl64, so the high half is masked alike for both widths;
+      // the low half is a full PM+32 word also at t = tl64 when B mod 8 >= 4
       const bool f64 = t < tl64;
-      if (t < 15) mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), f64 ? lo : 0u, f64 ? hi : 0u);  // Eq. (1)
+      const uint32_t hm = f64 ? hi : 0u;
+      if (t < 15) mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), f64 ? lo : 0u, hm);  // Eq. (1)
       mac32(C, K.a32[2 * t], 2 * t < tl32 ? lo : 0u);
-      if (t < 15) mac32(C, K.a32[2 * t + 1], 2 * t + 1 < tl32 ? hi : 0u);
+      if (t < 15) mac32(C, K.a32[2 * t + 1], hm);
     }
   }
   // marker words: the 8 bytes at 8 tl64, and its half holding byte 4 tl32
   const uint32_t z0 = fetch(2 * tl64), z1 = fetch(2 * tl64 + 1), z2 = fetch(2 * tl64 + 2);
   const uint32_t zl = funnel(z0, z1, sh), zh = funnel(z1, z2, sh);
-  const uint32_t r64 = B & 7, r32 = B & 3;
-  uint64_t w = ((uint64_t)zh << 32) | zl;
-  w = (w & ((1ULL << (8 * r64)) - 1)) | (1ULL << (8 * r64));
-  uint32_t w32 = r64 < 4 ? zl : zh;
-  w32 = (w32 & ((1u << (8 * r32)) - 1)) | (1u << (8 * r32));
+  // the partial 32-bit word is the PM+32 marker word, and a half of the PM+64 one
+  const bool up = (B & 4) != 0;                              // B mod 8 >= 4
+  const uint32_t mb = 1u << (8 * (B & 3));
+  const uint32_t w32 = ((up ? zh : zl) & (mb - 1)) | mb;
+  const uint64_t w = up ? ((uint64_t)w32 << 32) | zl : (uint64_t)w32;
   if (tl64 == 0) {
     lo64 = w;                                                // |sigma| = 1 (reading Q2)
   } else {
@@ -400,7 +403,21 @@ PMP_DI void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// (PMP_WAIT_HINT_NS > 0: try_wait with a suspend-time hint, so a waiting warp
+// sleeps until the phase completes instead of re-issuing the probe)
+#ifndef PMP_WAIT_HINT_NS
+#define PMP_WAIT_HINT_NS 0
+#endif
 PMP_DI void mbar_wait_s(uint32_t bar_s, uint32_t parity) {
+#if PMP_WAIT_HINT_NS
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "PMP_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra PMP_WAITS_%=;\n}" ::"r"(bar_s),
+      "r"(parity), "r"((uint32_t)PMP_WAIT_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P;\n"
       "PMP_WAITS_%=:\n\t"
@@ -408,6 +425,7 @@ PMP_DI void mbar_wait_s(uint32_t bar_s, uint32_t parity) {
       "@!P bra PMP_WAITS_%=;\n}" ::"r"(bar_s),
       "r"(parity)
       : "memory");
+#endif
 }
 PMP_DI void mbar_arrive_s(uint32_t bar_s) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_s) : "memory");
