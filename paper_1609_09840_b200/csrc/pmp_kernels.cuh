@@ -320,10 +320,9 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
 
 // Both digests of one short string in one pass (a 64-bit and a 32-bit key
 // schedule: the two configs[1] outputs).  The 32-bit words of PM+32 are the
-// halves of the 64-bit words of PM+64, so the loads, funnel shifts and the
-// loop are shared; each width keeps its own marker word, masks, exact sum and
-// reduction.  The loop covers the 64-bit words holding full 32-bit words,
-// (tf32 + 1) / 2 >= tlast64 of them, warp maximum tfull_max.
+// halves of the 64-bit words of PM+64, so the loads, funnel shifts, masks and
+// the loop over the full 64-bit words (warp maximum tfull_max) are shared;
+// each width keeps its own marker word, exact sum and reduction.
 template <class Fetch>
 PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ skeys, const uint32_t *__restrict__ skeys32,
                             uint32_t B, uint32_t sh, int tfull_max, Fetch fetch, uint64_t &lo64, uint32_t &lo32) {
@@ -342,13 +341,16 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
       const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
       const uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
       y0 = y2;
-      // 2t+1 < tl32 <=> t < tl64, so the high half is masked alike for both widths;
-      // the low half is a full PM+32 word also at t = tl64 when B mod 8 >= 4
+      // both halves of a full 64-bit word are full PM+32 words; the one PM+32
+      // word beyond them (the low half at t = tl64 when B mod 8 >= 4) is added
+      // with the markers below
       const bool f64 = t < tl64;
-      const uint32_t hm = f64 ? hi : 0u;
-      if (t < 15) mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), f64 ? lo : 0u, hm);  // Eq. (1)
-      mac32(C, K.a32[2 * t], 2 * t < tl32 ? lo : 0u);
-      if (t < 15) mac32(C, K.a32[2 * t + 1], hm);
+      const uint32_t lm = f64 ? lo : 0u, hm = f64 ? hi : 0u;
+      if (t < 15) {
+        mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lm, hm);  // Eq. (1)
+        mac32(C, K.a32[2 * t], lm);
+        mac32(C, K.a32[2 * t + 1], hm);
+      }
     }
   }
   // marker words: the 8 bytes at 8 tl64, and its half holding byte 4 tl32
@@ -359,6 +361,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   const uint32_t mb = 1u << (8 * (B & 3));
   const uint32_t w32 = ((up ? zh : zl) & (mb - 1)) | mb;
   const uint64_t w = up ? ((uint64_t)w32 << 32) | zl : (uint64_t)w32;
+  if (up) mac32(C, skeys32[2 * tl64], zl);                   // the full PM+32 word 2 tl64
   if (tl64 == 0) {
     lo64 = w;                                                // |sigma| = 1 (reading Q2)
   } else {
@@ -681,8 +684,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     }
 #endif
     // warp max of the number of full words (the marker word is handled apart)
-    const int tfm = DUAL ? (int)__reduce_max_sync(FULL, is_short ? ((B >> 2) + 1) >> 1 : 0u)
-                         : (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
+    const int tfm = (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
     if (is_short) {
       uint64_t lo;
       uint32_t lo32 = 0;
