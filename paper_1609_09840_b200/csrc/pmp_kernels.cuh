@@ -268,8 +268,10 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
       }
     }
     const uint32_t z0 = fetch(2 * tlast), z1 = fetch(2 * tlast + 1), z2 = fetch(2 * tlast + 2);
-    uint64_t w = ((uint64_t)funnel(z1, z2, sh) << 32) | funnel(z0, z1, sh);
-    w = (w & ((1ULL << (8 * r)) - 1)) | (1ULL << (8 * r));    // bytes || 0x01 || 0
+    const uint32_t zl = funnel(z0, z1, sh), zh = funnel(z1, z2, sh);
+    // bytes || 0x01 || 0: mask the half holding byte r, keep / drop the other
+    const uint32_t mb = 1u << (8 * (r & 3)), wh = (((r & 4) ? zh : zl) & (mb - 1)) | mb;
+    const uint64_t w = (r & 4) ? ((uint64_t)wh << 32) | zl : (uint64_t)wh;
     if (!V2 && tlast == 0) return w;                           // |sigma| = 1: no f_j (reading Q2)
     mac64(A, skeys[tlast], w);
     Acc5 x = macc_normalize(A);
