@@ -288,6 +288,7 @@ def main():
     outs = {}
     v2 = args.variant == "two-level"
     assert not (v2 and (args.buckets or args.stream_mib)), "--variant two-level: plain digests only"
+    fused_dual = False
     if wl.long:
         total = wl.lo
         begins = pmp.pmp_long_split(64, total, world)
@@ -350,6 +351,7 @@ def main():
         counts = torch.zeros(max(args.buckets, 1), dtype=torch.int32, device=dev)
 
         fused = len(wl.bits) == 2 and not v2 and not args.buckets and not args.separate_widths
+        fused_dual = fused
 
         def step():
             if fused:  # both outputs of the batch in one pass over the short strings (pmp_hash_batch_multi)
@@ -417,7 +419,7 @@ def main():
         peak, peak_src = hbm_peak()
         avg_ms = k_ms / max(k_cnt, 1)
         achieved = alg_bytes_per_launch / (avg_ms / 1000) / 1e9 if k_cnt else None
-        traffic = load_traffic(wl.name, dominant)
+        traffic = load_traffic(wl.name, dominant + ("+dual" if fused_dual else ""))
         clocks = clk.summary()
         cpu = None
         if not args.no_cpu:
