@@ -1060,6 +1060,9 @@ constexpr size_t kWBlockRegion = 1024 + 64 + 1024 + 512 + 1024 /* a_{1,0..127} *
 constexpr size_t kWSmem = kWBlockRegion + kWBlockWarps * kWSmemPerWarp;
 
 // Mid strings in 8-lane groups (mid_phase) instead of warp per string.
+#ifndef PMP_MID_INLINE
+#define PMP_MID_INLINE __noinline__
+#endif
 #ifndef PMP_MID_GROUPS
 #define PMP_MID_GROUPS 1
 #endif
@@ -1100,7 +1103,7 @@ constexpr size_t kMSmemPerWarp = ((size_t)kMStages * (4 * kMSlot + 4 * sizeof(MH
 // Runs after the warp has drained its big strings; uses the warp's shared
 // region (wbase) with its own ring layout and barriers.
 template <int BITS, bool POLY>
-__device__ __noinline__ void mid_phase(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
+__device__ PMP_MID_INLINE void mid_phase(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
                                        const uint64_t *__restrict__ offsets, const OutSpec &os,
                                        const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount,
                                        uint32_t nmid, const uint64_t *s_a2, const uint64_t *s_mklo,
@@ -1254,67 +1257,70 @@ __device__ __noinline__ void mid_phase(const uint64_t *__restrict__ keys, const 
     const uint64_t tlast = B / W;                   // marker word index
     const uint32_t rbytes = (uint32_t)(B % W);
     const uint64_t T1 = (tlast + 1 + 127) / 128;
-    // ---- this lane's 8 units of the group's piece, realigned to the string
+    // ---- this lane's 8 units of the group's piece, realigned to the string,
+    // in two halves of 4 units (fewer live registers: PM+32 halves are its two
+    // blocks), each multiply-added as soon as it is loaded
     const uint32_t ub = stg_s + (uint32_t)(q * 4 + g) * kMSlot + 16 * r;
-    uint4 U[8];
-    if (__all_sync(FULL, delta == 0)) {
-#pragma unroll
-      for (int j = 0; j < 8; j++)
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(U[j].x), "=r"(U[j].y), "=r"(U[j].z), "=r"(U[j].w) : "r"(ub + 128 * j));
-    } else {
-      const uint32_t a0 = ub + (delta & ~3u), sh = 8 * (delta & 3);
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const uint32_t a = a0 + 128 * j;
-        const uint32_t y0 = lds_u32(a), y1 = lds_u32(a + 4), y2 = lds_u32(a + 8), y3 = lds_u32(a + 12),
-                       y4 = lds_u32(a + 16);
-        U[j] = make_uint4(funnel(y0, y1, sh), funnel(y1, y2, sh), funnel(y2, y3, sh), funnel(y3, y4, sh));
-      }
-    }
+    const bool aligned = __all_sync(FULL, delta == 0);
     const uint64_t tw0 = (uint64_t)t * (kMPiece / W);  // first word of the piece
     const bool has_marker = active && tlast < tw0 + kMPiece / W;
-    if (__any_sync(FULL, has_marker || !active)) {
-      if (!active) {
-#pragma unroll
-        for (int j = 0; j < 8; j++) U[j] = make_uint4(0, 0, 0, 0);
-      } else if (has_marker) {
-#pragma unroll
-        for (int j = 0; j < 8; j++) fixup_unit<BITS>(U[j], tw0 + (uint64_t)(16 * (r + 8 * j)) / W, tlast, rbytes);
-      }
-    }
-    // ---- level-1 multiply-accumulate
+    const bool fix = __any_sync(FULL, has_marker || !active);
     Acc part[CPG];
-    if constexpr (BITS == 64) {
-      MacAcc64 A;
-      macc_zero(A);
+    MacAcc64 A64;
+    macc_zero(A64);
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        uint4 kk;  // a_{1,2u}, a_{1,2u+1}, u = r + 8j
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
-                     : "r"(a1_s + 16 * (r + 8 * j)));
-        mac64(A, kk.x, kk.y, U[j].x, U[j].y);
-        mac64(A, kk.z, kk.w, U[j].z, U[j].w);
-      }
-      part[0] = macc_normalize(A);
-    } else {
-      Acc3 A[2] = {{0, 0, 0}, {0, 0, 0}};
+    for (int hp = 0; hp < 2; hp++) {
+      uint4 U[4];
+      if (aligned) {
 #pragma unroll
-      for (int jj = 0; jj < 4; jj++) {
-        uint4 kk;  // a_{1,4u..4u+3}, u = r + 8 jj, the same for both blocks
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
-                     : "r"(a1_s + 16 * (r + 8 * jj)));
+        for (int j = 0; j < 4; j++)
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(U[j].x), "=r"(U[j].y), "=r"(U[j].z), "=r"(U[j].w) : "r"(ub + 128 * (4 * hp + j)));
+      } else {
+        const uint32_t a0 = ub + (delta & ~3u), sh = 8 * (delta & 3);
 #pragma unroll
-        for (int cs = 0; cs < 2; cs++) {
-          const uint4 &u = U[jj + 4 * cs];
-          mac32(A[cs], kk.x, u.x);
-          mac32(A[cs], kk.y, u.y);
-          mac32(A[cs], kk.z, u.z);
-          mac32(A[cs], kk.w, u.w);
+        for (int j = 0; j < 4; j++) {
+          const uint32_t a = a0 + 128 * (4 * hp + j);
+          const uint32_t y0 = lds_u32(a), y1 = lds_u32(a + 4), y2 = lds_u32(a + 8), y3 = lds_u32(a + 12),
+                         y4 = lds_u32(a + 16);
+          U[j] = make_uint4(funnel(y0, y1, sh), funnel(y1, y2, sh), funnel(y2, y3, sh), funnel(y3, y4, sh));
         }
       }
-      part[0] = A[0];
-      part[CPG - 1] = A[1];
+      if (fix) {
+        if (!active) {
+#pragma unroll
+          for (int j = 0; j < 4; j++) U[j] = make_uint4(0, 0, 0, 0);
+        } else if (has_marker) {
+#pragma unroll
+          for (int j = 0; j < 4; j++)
+            fixup_unit<BITS>(U[j], tw0 + (uint64_t)(16 * (r + 8 * (4 * hp + j))) / W, tlast, rbytes);
+        }
+      }
+      // ---- level-1 multiply-accumulate
+      if constexpr (BITS == 64) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          uint4 kk;  // a_{1,2u}, a_{1,2u+1}, u = r + 8j
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
+                       : "r"(a1_s + 16 * (r + 8 * (4 * hp + j))));
+          mac64(A64, kk.x, kk.y, U[j].x, U[j].y);
+          mac64(A64, kk.z, kk.w, U[j].z, U[j].w);
+        }
+        if (hp == 1) part[0] = macc_normalize(A64);
+      } else {
+        Acc3 A = {0, 0, 0};   // block hp of the piece
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          uint4 kk;  // a_{1,4u..4u+3}, u = r + 8 j, the same for both blocks
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
+                       : "r"(a1_s + 16 * (r + 8 * j)));
+          mac32(A, kk.x, U[j].x);
+          mac32(A, kk.y, U[j].y);
+          mac32(A, kk.z, U[j].z);
+          mac32(A, kk.w, U[j].w);
+        }
+        part[hp < CPG ? hp : 0] = A;
+      }
     }
     __syncwarp();
     consumed++;
