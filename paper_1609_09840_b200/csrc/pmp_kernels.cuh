@@ -1377,9 +1377,6 @@ __device__ PMP_MID_INLINE void mid_phase(const uint64_t *__restrict__ keys, cons
 }
 
 
-#ifndef PMP_W_EARLY
-#define PMP_W_EARLY 0
-#endif
 #ifndef PMP_W_MINB
 #define PMP_W_MINB 5
 #endif
@@ -1627,20 +1624,32 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     }
     const uint32_t st_s = stg_s + (uint32_t)q * kWStageBytes;
     const uint64_t c0 = (uint64_t)t * CPI;          // first level-1 block of this tile
-    uint4 U[8];
-    if (!nodata) {
-      const uint32_t ub = st_s + 1024 * g + 16 * r;  // this lane's unit j is at ub + 128 j (+ delta)
-      if (delta == 0) {                              // warp-uniform: aligned string
+    // ---- this lane's 8 units, in two halves of 4 (fewer live registers; the
+    // PM+32 halves are the group's two blocks), each multiply-added as loaded
+    Acc part[CPG];
+    const uint32_t ub = st_s + 1024 * g + 16 * r;    // this lane's unit j is at ub + 128 j (+ delta)
+    const bool tailtile = tlast < (c0 + CPI) * 128;   // warp-uniform: the tile holds the marker word
+    const uint64_t tw0 = (c0 + (uint64_t)g * CPG) * 128;
+    MacAcc64 A64;
+    macc_zero(A64);
 #pragma unroll
-        for (int j = 0; j < 8; j++)
+    for (int hp = 0; hp < 2; hp++) {
+      uint4 U[4];
+      if (nodata) {
+#pragma unroll
+        for (int j = 0; j < 4; j++) U[j] = make_uint4(0, 0, 0, 0);
+        // sigma of block c0 is (1, 0, ..., 0): its sum is a_{1,0} (added in lane 0 of group 0 below)
+      } else if (delta == 0) {                       // warp-uniform: aligned string
+#pragma unroll
+        for (int j = 0; j < 4; j++)
           asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(U[j].x), "=r"(U[j].y), "=r"(U[j].z), "=r"(U[j].w) : "r"(ub + 128 * j));
+                       : "=r"(U[j].x), "=r"(U[j].y), "=r"(U[j].z), "=r"(U[j].w) : "r"(ub + 128 * (4 * hp + j)));
       } else {                                       // realign: 5 aligned words + funnel shifts
         const uint32_t a0 = ub + (delta & ~3u), sh = 8 * (delta & 3);
         if ((delta & 4) == 0) {                      // a0 is 8-byte aligned: (y0,y1) (y2,y3) y4
 #pragma unroll
-          for (int j = 0; j < 8; j++) {
-            const uint32_t a = a0 + 128 * j;
+          for (int j = 0; j < 4; j++) {
+            const uint32_t a = a0 + 128 * (4 * hp + j);
             uint32_t y0, y1, y2, y3;
             lds_u32x2(a, y0, y1);
             lds_u32x2(a + 8, y2, y3);
@@ -1649,8 +1658,8 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
           }
         } else {                                     // a0 + 4 is 8-byte aligned: y0 (y1,y2) (y3,y4)
 #pragma unroll
-          for (int j = 0; j < 8; j++) {
-            const uint32_t a = a0 + 128 * j;
+          for (int j = 0; j < 4; j++) {
+            const uint32_t a = a0 + 128 * (4 * hp + j);
             uint32_t y1, y2, y3, y4;
             const uint32_t y0 = lds_u32(a);
             lds_u32x2(a + 4, y1, y2);
@@ -1659,64 +1668,42 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
           }
         }
       }
-      if (tlast < (c0 + CPI) * 128) {               // warp-uniform: the tile holds the marker word
-        const uint64_t tw0 = (c0 + (uint64_t)g * CPG) * 128;
+      if (!nodata && tailtile) {
 #pragma unroll
-        for (int j = 0; j < 8; j++) fixup_unit<BITS>(U[j], tw0 + (uint64_t)(16 * (r + 8 * j)) / W, tlast, rbytes);
+        for (int j = 0; j < 4; j++)
+          fixup_unit<BITS>(U[j], tw0 + (uint64_t)(16 * (r + 8 * (4 * hp + j))) / W, tlast, rbytes);
       }
-    }
-#if PMP_W_EARLY
-    // the tile is in registers: refill its slot before the multiply-adds
-    __syncwarp();
-    consumed++;
-    produce();
-#endif
-    // ---- level-1 multiply-accumulate (the hot loop) ----
-    Acc part[CPG];
-    if (nodata) {
-      // sigma of block c0 is (1, 0, ..., 0): its sum is a_{1,0} (added in lane 0 of group 0)
+      // ---- level-1 multiply-accumulate (the hot loop) ----
+      if constexpr (BITS == 64) {
 #pragma unroll
-      for (int cs = 0; cs < CPG; cs++) {
-        acc_zero(part[cs]);
-        if (lane == 0 && cs == 0) acc_add_word(part[cs], a10);
-      }
-    } else if constexpr (BITS == 64) {
-      MacAcc64 A;
-      macc_zero(A);
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        uint4 kk;  // a_{1,2u}, a_{1,2u+1} for this lane's unit u = r + 8j (block-shared copy)
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
-                     : "r"(a1_s + 16 * (r + 8 * j)));
-        mac64(A, kk.x, kk.y, U[j].x, U[j].y);
-        mac64(A, kk.z, kk.w, U[j].z, U[j].w);
-      }
-      part[0] = macc_normalize(A);
-    } else {
-      Acc3 A[2] = {{0, 0, 0}, {0, 0, 0}};
-#pragma unroll
-      for (int jj = 0; jj < 4; jj++) {
-        uint4 kk;  // a_{1,4u..4u+3}, u = r + 8 jj (packed u32 copy), same for both blocks
-        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
-                     : "r"(a1_s + 16 * (r + 8 * jj)));
-#pragma unroll
-        for (int cs = 0; cs < 2; cs++) {
-          const uint4 &u = U[jj + 4 * cs];
-          mac32(A[cs], kk.x, u.x);
-          mac32(A[cs], kk.y, u.y);
-          mac32(A[cs], kk.z, u.z);
-          mac32(A[cs], kk.w, u.w);
+        for (int j = 0; j < 4; j++) {
+          uint4 kk;  // a_{1,2u}, a_{1,2u+1} for this lane's unit u = r + 8j (block-shared copy)
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
+                       : "r"(a1_s + 16 * (r + 8 * (4 * hp + j))));
+          mac64(A64, kk.x, kk.y, U[j].x, U[j].y);
+          mac64(A64, kk.z, kk.w, U[j].z, U[j].w);
         }
+        if (hp == 1) part[0] = macc_normalize(A64);
+      } else {
+        Acc3 A = {0, 0, 0};   // block hp of the group block
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          uint4 kk;  // a_{1,4u..4u+3}, u = r + 8 j (packed u32 copy), same for both blocks
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(kk.x), "=r"(kk.y), "=r"(kk.z), "=r"(kk.w)
+                       : "r"(a1_s + 16 * (r + 8 * j)));
+          mac32(A, kk.x, U[j].x);
+          mac32(A, kk.y, U[j].y);
+          mac32(A, kk.z, U[j].z);
+          mac32(A, kk.w, U[j].w);
+        }
+        part[hp < CPG ? hp : 0] = A;
       }
-      part[0] = A[0];
-      part[CPG - 1] = A[1];
     }
-#if !PMP_W_EARLY
+    if (nodata && lane == 0) acc_add_word(part[0], a10);
     __syncwarp();
     // the slot is free: refill the ring before the reductions
     consumed++;
     produce();
-#endif
     // POLY: virtual node of the tile's first chunk, and whether the tile crosses
     // into the next one (virtual node boundaries fall inside tiles when d > 0)
     const uint64_t qf = (c0 + dsh) >> 7;
