@@ -397,7 +397,7 @@ def main():
     launches = pmp.pmp_launch_count() - l0
     ms = ev0.elapsed_time(ev1)
     k_ms, k_cnt = pmp.pmp_prof_read(dominant)
-    kernel_ms = {name: pmp.pmp_prof_read(name) for name in ("k_short", "k_wstring", "k_node", "k_level", "k_combine",
+    kernel_ms = {name: pmp.pmp_prof_read(name) for name in ("k_short", "k_wstring", "k_histogram", "k_node", "k_level", "k_combine",
                                                              "k_stream", "k_poly")}
     t = torch.tensor([ms], dtype=torch.float64, device=cdev)
     if world > 1:

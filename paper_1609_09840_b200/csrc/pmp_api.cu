@@ -752,8 +752,15 @@ int pmp_hash_batch_buckets(const pmp_keys *k, const uint8_t *bytes, const uint64
   OutSpec os;
   os.out = buckets;
   os.M = M;
-  os.counts = counts;
-  return hash_batch_impl(k, bytes, offsets, n, os, st);
+  os.counts = nullptr;   // counted by k_histogram below, not by atomics in the hash kernels
+  if (int rc = hash_batch_impl(k, bytes, offsets, n, os, st)) return rc;
+  if (!counts || n == 0) return 0;
+  const int sms = sm_count(k->device);
+  const size_t smem = M <= kHistSmemMax ? (size_t)M * 4 : 0;
+  uint64_t grid = (n + 511) / 512;
+  if (grid > (uint64_t)sms * 4) grid = (uint64_t)sms * 4;
+  return launch("k_histogram", st,
+                [&] { k_histogram<<<(unsigned)grid, 512, smem, st>>>(buckets, n, M, counts); });
 }
 
 int pmp_hash_batch_multi(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,

@@ -2267,6 +2267,32 @@ __global__ void k_combine(const uint64_t *__restrict__ partials, int G, uint64_t
 //         in = [b, a_0..a_127, s_0..s_127], out = (lo, hi).
 // mode 2: out = mix(in[0]).
 // mode 3: as mode 0 but only (value mod p) mod 2^n (the digest input).
+// Histogram of bucket ids (the hash-table consumer's counts):
+// a separate pass over the n bucket ids, privatised per block in shared memory
+// when M fits (one global atomic per non-empty bucket and block), so the
+// hashing kernels never contend on a few hundred global counters.
+constexpr uint32_t kHistSmemMax = 12288;     // counters per block (48 KB)
+__global__ void __launch_bounds__(512)
+k_histogram(const uint32_t *__restrict__ buckets, uint64_t n, uint32_t M, uint32_t *__restrict__ counts) {
+  extern __shared__ uint32_t h[];
+  const bool priv = M <= kHistSmemMax;
+  if (priv) {
+    for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+  }
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t b = __ldcs(buckets + i);
+    if (priv) atomicAdd(&h[b], 1u);
+    else atomicAdd(&counts[b], 1u);
+  }
+  if (priv) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < M; i += blockDim.x)
+      if (h[i]) atomicAdd(&counts[i], h[i]);
+  }
+}
+
 template <int BITS>
 __global__ void k_selftest(int mode, const uint64_t *__restrict__ in, uint64_t n, uint64_t *__restrict__ outv) {
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;

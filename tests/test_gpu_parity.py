@@ -296,7 +296,7 @@ def test_long_partition_invariance(torch_dev, oracle_lib, bits):
 
 # ------------------------------------------------------------ hash-table consumer
 @pytest.mark.parametrize("bits", [32, 64])
-@pytest.mark.parametrize("M", [1, 7, 1024, 2**32 - 1])
+@pytest.mark.parametrize("M", [1, 7, 1024, 50_000, 2**32 - 1])   # 50,000: histogram without the smem copy
 def test_buckets_and_histogram(torch_dev, oracle_lib, bits, M):
     """pmp_hash_batch_buckets == oracle digest mod M, and its fused histogram ==
     bincount, for a batch mixing short, long, empty and misaligned strings."""
