@@ -350,13 +350,14 @@ def main():
 
         counts = torch.zeros(max(args.buckets, 1), dtype=torch.int32, device=dev)
 
-        fused = len(wl.bits) == 2 and not v2 and not args.buckets and not args.separate_widths
+        fused = len(wl.bits) == 2 and not args.buckets and not args.separate_widths
         fused_dual = fused
+        multi_fn = pmp.pmp_hash2_batch_multi if v2 else pmp.pmp_hash_batch_multi
 
         def step():
             if fused:  # both outputs of the batch in one pass over the short strings (pmp_hash_batch_multi)
-                pmp._check(pmp.pmp_hash_batch_multi([keys[b].handle for b in wl.bits], d_pay.data_ptr(),
-                                                    d_off.data_ptr(), n, [outs[b].data_ptr() for b in wl.bits], sp),
+                pmp._check(multi_fn([keys[b].handle for b in wl.bits], d_pay.data_ptr(),
+                                    d_off.data_ptr(), n, [outs[b].data_ptr() for b in wl.bits], sp),
                            "pmp_hash_batch_multi")
                 return
             for b in wl.bits:

@@ -208,6 +208,7 @@ void pmp_stream_free(pmp_stream *s);
  * digests from the tree.  Conventions, arguments and errors are those of the
  * tree calls of the same shape:
  *   pmp_hash2_batch        ~ pmp_hash_batch
+ *   pmp_hash2_batch_multi  ~ pmp_hash_batch_multi (a 64- and a 32-bit schedule fused likewise)
  *   pmp_hash2_long         ~ pmp_hash_long
  *   pmp_hash2_long_partial ~ pmp_hash_long_partial: the caller's chunks
  *       contribute sum v_c r^(C-c) (a field element, 2 words) -- no key-only
@@ -215,6 +216,8 @@ void pmp_stream_free(pmp_stream *s);
  *   pmp_hash2_long_combine: digest of b_2 + sum_g P_g (G partials, device). */
 int pmp_hash2_batch(const pmp_keys *keys, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
                     void *out, struct CUstream_st *stream);
+int pmp_hash2_batch_multi(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
+                          uint64_t n, void *const *outs, struct CUstream_st *stream);
 int pmp_hash2_long(const pmp_keys *keys, const uint8_t *bytes, uint64_t len, void *out,
                    struct CUstream_st *stream);
 int pmp_hash2_long_partial(const pmp_keys *keys, const uint8_t *local, uint64_t local_len,

@@ -53,6 +53,7 @@ def lib() -> ctypes.CDLL:
             "pmp_hash_batch_buckets": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _vp, _vp], _int),
             "pmp_hash_batch_host": ([_vp, _int, _vp, _vp, _u64, _vp, _u64, _vp], _int),
             "pmp_hash_batch_multi": ([_vp, _int, _vp, _vp, _u64, _vp, _vp], _int),
+            "pmp_hash2_batch_multi": ([_vp, _int, _vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_long": ([_vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_long_partial": ([_vp, _vp, _u64, _u64, _u64, _vp, _vp], _int),
             "pmp_hash_long_combine": ([_vp, _vp, _int, _u64, _vp, _vp], _int),
@@ -132,6 +133,13 @@ def pmp_hash_batch_multi(keys: list, bytes_ptr: int, offsets_ptr: int, n: int, o
     ka = (_vp * len(keys))(*keys)
     oa = (_vp * len(out_ptrs))(*out_ptrs)
     return lib().pmp_hash_batch_multi(ka, len(keys), bytes_ptr, offsets_ptr, n, oa, stream)
+
+
+def pmp_hash2_batch_multi(keys: list, bytes_ptr: int, offsets_ptr: int, n: int, out_ptrs: list, stream: int) -> int:
+    """pmp_hash_batch_multi for the two-level variant."""
+    ka = (_vp * len(keys))(*keys)
+    oa = (_vp * len(out_ptrs))(*out_ptrs)
+    return lib().pmp_hash2_batch_multi(ka, len(keys), bytes_ptr, offsets_ptr, n, oa, stream)
 
 
 def pmp_hash_batch_host(keys: list, bytes_ptr: int, offsets_ptr: int, n: int, out_ptrs: list,

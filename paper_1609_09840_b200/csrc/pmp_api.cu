@@ -667,7 +667,7 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   if (!bytes || !offsets || !os.out || n >= (1ULL << 32)) return PMP_EINVAL;
   if (int rc = check_keys(k)) return rc;
   const bool dual = k2 != nullptr;
-  if (dual && (!os2 || !os2->out || v2 || k->bits != 64 || k2->bits != 32 || k2->device != k->device))
+  if (dual && (!os2 || !os2->out || k->bits != 64 || k2->bits != 32 || k2->device != k->device))
     return PMP_EINVAL;
   const int sms = sm_count(k->device);
   Scratch sc(st), sc_off(st);
@@ -680,11 +680,14 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   if (dual) {
     for (int i = 0; i < 32; i++) pk.a32[i] = (uint32_t)k2->a[i];
     pk.b32 = k2->b[0];
+    pk.r32 = k2->a[kM];   // a_{2,1}
+    pk.b2_32 = k2->b[1];
   }
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    const void *fs[5] = {(const void *)k_short<64>, (const void *)k_short<32>, (const void *)k_short<64, true>,
-                         (const void *)k_short<32, true>, (const void *)k_short<64, false, true>};
+    const void *fs[6] = {(const void *)k_short<64>, (const void *)k_short<32>, (const void *)k_short<64, true>,
+                         (const void *)k_short<32, true>, (const void *)k_short<64, false, true>,
+                         (const void *)k_short<64, true, true>};
     for (const void *f : fs) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
@@ -703,7 +706,7 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     offsets = (const uint64_t *)al;
   }
   // ---- short strings (and the work list of long ones)
-  const void *kshort = dual ? (const void *)k_short<64, false, true>
+  const void *kshort = dual ? (v2 ? (const void *)k_short<64, true, true> : (const void *)k_short<64, false, true>)
                             : v2 ? (k->bits == 64 ? (const void *)k_short<64, true> : (const void *)k_short<32, true>)
                                  : (k->bits == 64 ? (const void *)k_short<64> : (const void *)k_short<32>);
   const int threads = (kShortWarps + 1) * 32;  // + producer warp
@@ -763,8 +766,8 @@ int pmp_hash_batch_buckets(const pmp_keys *k, const uint8_t *bytes, const uint64
                 [&] { k_histogram<<<(unsigned)grid, 512, smem, st>>>(buckets, n, M, counts); });
 }
 
-int pmp_hash_batch_multi(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
-                         uint64_t n, void *const *outs, cudaStream_t st) {
+static int batch_multi_impl(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
+                            uint64_t n, void *const *outs, cudaStream_t st, bool v2) {
   if (!keys || !outs || nkeys < 1 || nkeys > PMP_HOST_MAX_KEYS) return PMP_EINVAL;
   for (int k = 0; k < nkeys; k++)
     if (!keys[k] || !outs[k]) return PMP_EINVAL;
@@ -775,16 +778,27 @@ int pmp_hash_batch_multi(const pmp_keys *const *keys, int nkeys, const uint8_t *
     for (int j = 0; j < nkeys; j++) {
       if (done[j] || keys[j]->bits != 32 || keys[j]->device != keys[k]->device) continue;
       OutSpec a{outs[k], 0, nullptr}, b{outs[j], 0, nullptr};
-      if (int rc = hash_batch_impl(keys[k], bytes, offsets, n, a, st, false, keys[j], &b)) return rc;
+      if (int rc = hash_batch_impl(keys[k], bytes, offsets, n, a, st, v2, keys[j], &b)) return rc;
       done[k] = done[j] = true;
       break;
     }
   }
   for (int k = 0; k < nkeys; k++) {
     if (done[k]) continue;
-    if (int rc = pmp_hash_batch(keys[k], bytes, offsets, n, outs[k], st)) return rc;
+    OutSpec a{outs[k], 0, nullptr};
+    if (int rc = hash_batch_impl(keys[k], bytes, offsets, n, a, st, v2)) return rc;
   }
   return 0;
+}
+
+int pmp_hash_batch_multi(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
+                         uint64_t n, void *const *outs, cudaStream_t st) {
+  return batch_multi_impl(keys, nkeys, bytes, offsets, n, outs, st, false);
+}
+
+int pmp_hash2_batch_multi(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
+                          uint64_t n, void *const *outs, cudaStream_t st) {
+  return batch_multi_impl(keys, nkeys, bytes, offsets, n, outs, st, true);
 }
 
 // Host-resident batches: string-aligned pieces streamed through the device on

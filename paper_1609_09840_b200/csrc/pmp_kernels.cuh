@@ -50,6 +50,7 @@ struct ParamKeys {
   // dual-width k_short: the 32-bit schedule's a_{1,0..31} and b_1 (a, b hold the 64-bit one)
   uint32_t a32[32];
   uint64_t b32;
+  uint64_t r32, b2_32;  // and its two-level r = a_{2,1}, b_2
 };
 
 // ------------------------------------------------------------- helpers
@@ -325,7 +326,9 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
 // halves of the 64-bit words of PM+64, so the loads, funnel shifts, masks and
 // the loop over the full 64-bit words (warp maximum tfull_max) are shared;
 // each width keeps its own marker word, exact sum and reduction.
-template <class Fetch>
+// V2: the two-level variant (reading Q19) for both schedules: V = b_2 + r v_0,
+// every string (no |sigma| = 1 shortcut).
+template <bool V2, class Fetch>
 PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ skeys, const uint32_t *__restrict__ skeys32,
                             uint32_t B, uint32_t sh, int tfull_max, Fetch fetch, uint64_t &lo64, uint32_t &lo32) {
   const int tl64 = (int)(B >> 3), tl32 = (int)(B >> 2);
@@ -364,20 +367,36 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   const uint32_t w32 = ((up ? zh : zl) & (mb - 1)) | mb;
   const uint64_t w = up ? ((uint64_t)w32 << 32) | zl : (uint64_t)w32;
   if (up) mac32(C, skeys32[2 * tl64], zl);                   // the full PM+32 word 2 tl64
-  if (tl64 == 0) {
+  if (!V2 && tl64 == 0) {
     lo64 = w;                                                // |sigma| = 1 (reading Q2)
   } else {
     mac64(A, skeys[tl64], w);
     Acc5 x = macc_normalize(A);
     acc5_add_u64(x, K.b);
-    lo64 = reduce_lo_acc5(x);
+    if constexpr (V2) {
+      const Fe64 v0 = reduce_acc5(x);
+      Acc5 y = {0, 0, 0, 0, 0};
+      acc5_mac_fe(y, K.r, v0);
+      acc5_add_u64(y, K.b2);
+      lo64 = reduce_lo_acc5(y);
+    } else {
+      lo64 = reduce_lo_acc5(x);
+    }
   }
-  if (tl32 == 0) {
+  if (!V2 && tl32 == 0) {
     lo32 = w32;
   } else {
     mac32(C, skeys32[tl32], w32);
     acc3_add_u64(C, K.b32);
-    lo32 = reduce_lo_acc3(C);
+    if constexpr (V2) {
+      const uint64_t v0 = reduce_acc3(C);
+      Acc3 y = {0, 0, 0};
+      acc3_mac_fe(y, (uint32_t)K.r32, v0);
+      acc3_add_u64(y, K.b2_32);
+      lo32 = reduce_lo_acc3(y);
+    } else {
+      lo32 = reduce_lo_acc3(C);
+    }
   }
 }
 
@@ -695,7 +714,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         const uint32_t sofs = rpos + (valid ? (uint32_t)((uintptr_t)(bytes + o0) - (uintptr_t)ralo) : 0u);
         const uint32_t pa = ring_s + (sofs & ~3u);
         auto fetch = [&](int kk) { return lds_u32(pa + 4 * kk); };
-        if constexpr (DUAL) short_tree_dual(K, skeys, skeys32, B, 8 * (sofs & 3), tfm, fetch, lo, lo32);
+        if constexpr (DUAL) short_tree_dual<V2>(K, skeys, skeys32, B, 8 * (sofs & 3), tfm, fetch, lo, lo32);
         else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (sofs & 3), tfm, fetch);
       } else {
         // direct tile: read the string's aligned 32-bit words straight from global,
@@ -706,7 +725,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
           const uintptr_t a = pa + 4 * (uintptr_t)kk;
           return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
         };
-        if constexpr (DUAL) short_tree_dual(K, skeys, skeys32, B, 8 * (uint32_t)(sa & 3), tfm, fetch, lo, lo32);
+        if constexpr (DUAL) short_tree_dual<V2>(K, skeys, skeys32, B, 8 * (uint32_t)(sa & 3), tfm, fetch, lo, lo32);
         else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, fetch);
       }
       if (valid) {

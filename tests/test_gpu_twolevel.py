@@ -172,3 +172,32 @@ def test_hash2_power_above_2n(dev, oracle_lib, bits):
     off = datagen.offsets_from_lengths(lens)
     pay = datagen.payload_host(57, 0, int(off[-1]))
     assert np.array_equal(_batch(dev, keys, pay, off), _want(oracle_lib, okeys, pay, off))
+
+
+@pytest.mark.parametrize("order", [(64, 32), (32, 64)])
+def test_hash2_multi_fused(dev, oracle_lib, order):
+    """pmp_hash2_batch_multi: the two-level variant under a 64- and a 32-bit
+    schedule in one fused pass over the short strings (every length 0..300,
+    T = 1 strings included, all alignments) plus long members."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    lens = np.concatenate([np.repeat(np.arange(0, 301), 3), [5000, 70_000, 1024, 0]]).astype(np.uint64)
+    rng.shuffle(lens)
+    off = datagen.offsets_from_lengths(lens) + 5
+    pay = datagen.payload_host(71, 0, int(off[-1]))
+    seeds = [71, 72]
+    keys = [pmp.Keys.generate(s, b) for s, b in zip(seeds, order)]
+    d_pay = torch.from_numpy(pay).to(dev)
+    d_off = torch.from_numpy(off.view(np.int64)).to(dev)
+    n = lens.size
+    outs = [torch.empty(n, dtype=torch.int64 if b == 64 else torch.int32, device=dev) for b in order]
+    rc = pmp.pmp_hash2_batch_multi([k.handle for k in keys], d_pay.data_ptr(), d_off.data_ptr(), n,
+                                   [o.data_ptr() for o in outs], 0)
+    assert rc == 0
+    torch.cuda.synchronize()
+    for s, b, o in zip(seeds, order, outs):
+        got = pmp.as_u64(o).astype(np.uint64)
+        want = _want(oracle_lib, oracle_lib.keygen(s, b), pay, off)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (b, [(int(i), int(lens[i])) for i in bad[:8]])
