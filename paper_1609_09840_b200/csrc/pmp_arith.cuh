@@ -221,27 +221,27 @@ PMP_HDI Fe64 alg2_64(uint64_t v0, uint32_t v1) {
   return z;
 }
 
-// V mod 2^64 only (the digest input), same arithmetic as Section 6.2 +
-// Algorithm 2 with the branches folded:
-//   v = (w0 - u0) + (k^2 w2 + k u1 + k) + 2^64, so with d = w0 - u0 (borrow bw)
-//   and e = d + t (carry ce): v0 = e, v1 = ce + 1 - bw;
-//   Alg. 2 (corrected) gives lo = v0 - k v1 + k [v0 < k v1]  (mod 2^64):
-//   case k v1 <= v0 -> v0 - k v1; case v1 = 1, v0 < k -> v0 (hi = 1);
-//   case v1 = 2, v0 < 2k -> v0 - k (mod 2^64, hi = [v0 >= k]).
+// V mod 2^64 only (the digest input) of S = w0 + w1 2^64 + w2 2^128
+// (w2 < 2^24), by the same congruences as Section 6.2 (2^64 = -k, 2^128 = k^2
+// mod p), folded so that no 64x64 product is formed:
+//   -k w1 = k ~w1 + k - k 2^64 = k ~w1 + k + k^2  (mod p),  ~w1 = 2^64 - 1 - w1,
+//   so S = Y := w0 + k ~w1 + k^2 w2 + k^2 + k, with Y = y0 + y1 2^64, y1 <= 14;
+//   S = y0 - k y1 (mod p), and y0 - k y1 is in [-(k^2 + k), 2^64): if it is
+//   negative, V = y0 - k y1 + p and V mod 2^64 = y0 - k y1 + k (mod 2^64).
+// Equal to the 3->2 reduction followed by Algorithm 2 (corrected, reading Q6)
+// and taking the low word: checked on the device against the oracle
+// (test_reduction_fuzz_and_algorithm2_branches, mode 3).
 PMP_HDI uint64_t reduce_lo_words64(uint64_t w0, uint64_t w1, uint64_t w2) {
-#ifdef __CUDA_ARCH__
-  const uint64_t u1 = __umul64hi(w1, kK64);
-#else
-  const uint64_t u1 = (uint64_t)(((unsigned __int128)w1 * kK64) >> 64);
-#endif
-  const uint64_t u0 = w1 * kK64;
-  const uint64_t t = kK64 * kK64 * w2 + kK64 * u1 + kK64;
-  const uint64_t d = w0 - u0;
-  const uint64_t bw = w0 < u0;
-  const uint64_t e = d + t;
-  const uint64_t v1 = (uint64_t)(e < t) + 1 - bw;
-  const uint64_t kv = kK64 * v1;
-  return e - kv + (e < kv ? kK64 : 0);
+  const uint32_t K = (uint32_t)w2 * (uint32_t)(kK64 * kK64) + (uint32_t)(kK64 * kK64 + kK64);
+  const uint64_t A = (uint64_t)(~(uint32_t)w1) * kK64 + K;            // k ~w1_lo + k^2 w2 + k^2 + k
+  const uint64_t Bm = (uint64_t)(~(uint32_t)(w1 >> 32)) * kK64;       // k ~w1_hi (weight 2^32)
+  uint64_t y0 = w0 + A;
+  uint32_t y1 = y0 < A;
+  const uint64_t bs = Bm << 32;
+  y0 += bs;
+  y1 += (uint32_t)(y0 < bs) + (uint32_t)(Bm >> 32);
+  const uint64_t kv = kK64 * y1;
+  return y0 - kv + (y0 < kv ? kK64 : 0);
 }
 PMP_HDI uint64_t reduce_lo_acc5(const Acc5 &x) {
   return reduce_lo_words64(((uint64_t)x.c1 << 32) | x.c0, ((uint64_t)x.c3 << 32) | x.c2, x.c4);
