@@ -421,6 +421,7 @@ def main():
         avg_ms = k_ms / max(k_cnt, 1)
         achieved = alg_bytes_per_launch / (avg_ms / 1000) / 1e9 if k_cnt else None
         traffic = load_traffic(wl.name, dominant + ("+dual" if fused_dual else ""))
+        pipes = load_traffic(wl.name, dominant + ("+dual" if fused_dual else ""), "pipes.json")
         clocks = clk.summary()
         cpu = None
         if not args.no_cpu:
@@ -440,7 +441,10 @@ def main():
                          "peak_source": peak_src, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes_per_launch, "avg_launch_ms": avg_ms,
-                         "launches_timed": k_cnt},
+                         "launches_timed": k_cnt,
+                         # integer-pipe / issue utilisation of this kernel from the committed
+                         # ncu capture (profiles/pipes.json), for the IMAD side of the roofline
+                         "ncu_pipes": pipes},
             "clocks": clocks,
             "gpu_launches": launches,
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in kernel_ms.items() if v[1]},
@@ -527,8 +531,8 @@ def cpu_baseline(wl, variant="tree"):
         return {"value": None, "unit": "GB/s", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
 
 
-def load_traffic(workload, kernel):
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+def load_traffic(workload, kernel, name="traffic.json"):
+    path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as f:
             return json.load(f).get(workload, {}).get(kernel)
