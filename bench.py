@@ -211,7 +211,8 @@ def run_reference(args, wl):
             "ms_per_step": 1000 * statistics.median(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64+u32" if len(wl.bits) > 1 else f"u{wl.bits[0]}",
             "data": "synthetic (seeded xoshiro256** bytes)", "config": workload_config(wl, args.gpus, args.variant),
-            "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "oracle", "sample": desc,
+                             "host": host_cpu()},
             "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -526,9 +527,24 @@ def cpu_baseline(wl, variant="tree"):
             v, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=10.0, base=b0,
                                                     variant=variant)
         return {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc,
-                "seconds": dt}
+                "seconds": dt, "host": host_cpu()}
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "GB/s", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
+
+
+def host_cpu():
+    """CPU model, logical CPUs and sockets of the host the oracle ran on."""
+    model, sockets = None, set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name") and model is None:
+                    model = ln.split(":", 1)[1].strip()
+                elif ln.startswith("physical id"):
+                    sockets.add(ln.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count(), "sockets": len(sockets) or None}
 
 
 def load_traffic(workload, kernel, name="traffic.json"):
