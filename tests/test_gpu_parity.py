@@ -462,3 +462,41 @@ def test_multi_schedule_fused_pass(torch_dev, oracle_lib, order):
         want = oracle_batch(oracle_lib, s, b, pay, off)
         bad = np.nonzero(got != want)[0]
         assert bad.size == 0, (b, [(int(i), int(lens[i])) for i in bad[:8]])
+
+
+@pytest.mark.parametrize("trial", range(32))
+def test_random_batches_soak(torch_dev, oracle_lib, trial):
+    """Randomised batches through every batch entry point (pmp_hash_batch,
+    the fused two-schedule pmp_hash_batch_multi, the host-resident path):
+    random count, length law (short / mid / big / mixed), payload shift, key
+    seeds; bit-exact against the oracle."""
+    import torch
+
+    rng = np.random.default_rng(1000 + trial)
+    n = int(rng.integers(1, 4000))
+    law = trial % 4
+    if law == 0:
+        lens = rng.integers(0, 128, size=n)
+    elif law == 1:
+        lens = np.floor(2.0 ** rng.uniform(7, 16, size=n))
+    elif law == 2:
+        n = int(rng.integers(1, 40))
+        lens = np.floor(2.0 ** rng.uniform(16, 19, size=n))
+    else:
+        lens = np.floor(2.0 ** rng.uniform(0, 18, size=n))
+    lens = lens.astype(np.uint64)
+    off = datagen.offsets_from_lengths(lens) + int(rng.integers(0, 16))
+    pay = datagen.payload_host(int(rng.integers(1, 1 << 30)), 0, int(off[-1]))
+    s64, s32 = int(rng.integers(1, 1 << 40)), int(rng.integers(1, 1 << 40))
+    k64, k32 = pmp.Keys.generate(s64, 64), pmp.Keys.generate(s32, 32)
+    want64 = oracle_batch(oracle_lib, s64, 64, pay, off)
+    want32 = oracle_batch(oracle_lib, s32, 32, pay, off)
+    d_pay = torch.from_numpy(pay if pay.size else np.zeros(16, np.uint8)).to(torch_dev)
+    d_off = torch.from_numpy(off.view(np.int64)).to(torch_dev)
+    o64, o32 = pmp.hash_batch_multi([k64, k32], d_pay, d_off)
+    torch.cuda.synchronize()
+    assert np.array_equal(pmp.as_u64(o64), want64)
+    assert np.array_equal(pmp.as_u64(o32), want32)
+    assert np.array_equal(run_batch(torch_dev, k64, pay, off), want64)
+    h64, h32 = pmp.hash_batch_host([k64, k32], pay, off, piece_bytes=int(rng.integers(1, 1 << 20)))
+    assert np.array_equal(h64, want64) and np.array_equal(h32, want32)
