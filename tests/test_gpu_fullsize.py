@@ -85,6 +85,31 @@ def test_hashtable_full_size_sampled(dev, oracle_lib, bits):
     _check_sample(oracle_lib, oracle_lib.keygen(wl.seed, bits), wl.seed, offs, got, idx)
 
 
+def test_hashtable_full_size_fused_both_widths(dev, oracle_lib):
+    """configs[1] in bench.py's launch configuration: both widths in one fused
+    pass (pmp_hash_batch_multi); 20,000 random + first/last 500 digests of
+    each width recomputed by the oracle, and both equal the per-width launches
+    on a further 100,000 indices."""
+    import torch
+
+    wl = datagen.WORKLOADS["hashtable"]
+    offs = datagen.offsets_from_lengths(wl.lengths())
+    pay, d_off = _device_batch(dev, wl.seed, offs)
+    k64, k32 = pmp.Keys.generate(wl.seed, 64), pmp.Keys.generate(wl.seed, 32)
+    o64, o32 = pmp.hash_batch_multi([k64, k32], pay, d_off)
+    s64 = pmp.hash_batch(k64, pay, d_off)
+    s32 = pmp.hash_batch(k32, pay, d_off)
+    torch.cuda.synchronize()
+    g64, g32 = pmp.as_u64(o64), pmp.as_u64(o32)
+    n = wl.n
+    rng = np.random.default_rng(64 + 32)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 20000), np.arange(500), np.arange(n - 500, n)]))
+    _check_sample(oracle_lib, oracle_lib.keygen(wl.seed, 64), wl.seed, offs, g64, idx)
+    _check_sample(oracle_lib, oracle_lib.keygen(wl.seed, 32), wl.seed, offs, g32, idx)
+    j = rng.integers(0, n, 100000)
+    assert np.array_equal(g64[j], pmp.as_u64(s64)[j]) and np.array_equal(g32[j], pmp.as_u64(s32)[j])
+
+
 def test_fixed4k_full_size_sampled(dev, oracle_lib):
     """configs[2]: 2^20 x 4096 B (4 GiB), PM+64, seed 3; 3,000 sampled digests."""
     import torch
