@@ -168,6 +168,46 @@ def oracle_sample_rate(wl, seed, offs, bits_list, budget_s=12.0, max_threads=Non
     return nbytes / dt / 1e9, threads, f"first {n_s} strings of the batch ({int(offs[n_s])} B), widths {bits_list}", dt
 
 
+def oracle_single_thread(wl, variant="tree", budget_s=2.0):
+    """One host thread of the oracle on a small sample of the workload (SURVEY
+    8(d): a single-core figure beside the paper's bytes/cycle/core; the oracle
+    is the literal slow program, not the paper's tuned code)."""
+    import oracle
+
+    bits = wl.bits[0]
+    k = oracle.keygen(wl.seed, bits)
+    if wl.long:
+        nb = 8 << 20
+        pay = datagen.payload_host(wl.seed, 0, nb)
+        t0 = time.perf_counter()
+        (oracle.hash2 if variant == "two-level" else oracle.hash_long)(k, pay, nthreads=1)
+        dt = time.perf_counter() - t0
+    else:
+        lens = wl.lengths()[: 1 << 16].astype(np.uint64)
+        offs = datagen.offsets_from_lengths(lens)
+        n = 1 << 16
+        if wl.name in ("mixed", "fixed4k"):
+            n = min(n, int(np.searchsorted(offs, 32 << 20)))
+        offs = offs[: n + 1]
+        pay = datagen.payload_host(wl.seed, 0, int(offs[-1]))
+        t0 = time.perf_counter()
+        (oracle.hash2_batch if variant == "two-level" else oracle.hash_batch)(k, pay, offs, nthreads=1)
+        dt = time.perf_counter() - t0
+        nb = int(offs[-1])
+    mhz = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("cpu MHz"):
+                    mhz = float(ln.split(":", 1)[1])
+                    break
+    except OSError:
+        pass
+    gbs = nb / dt / 1e9
+    return {"value": gbs, "unit": "GB/s", "width": bits, "sample_bytes": nb,
+            "bytes_per_cycle": (gbs * 1e9 / (mhz * 1e6)) if mhz else None, "cpu_mhz": mhz}
+
+
 def oracle_long_rate(wl, nbytes_sample, budget_s=12.0, variant="tree"):
     import oracle
 
@@ -527,7 +567,7 @@ def cpu_baseline(wl, variant="tree"):
             v, cores, desc, dt = oracle_sample_rate(wl, seed, offs, list(wl.bits), budget_s=10.0, base=b0,
                                                     variant=variant)
         return {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc,
-                "seconds": dt, "host": host_cpu()}
+                "seconds": dt, "host": host_cpu(), "single_thread": oracle_single_thread(wl, variant)}
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "GB/s", "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
 
