@@ -770,7 +770,10 @@ static int batch_multi_impl(const pmp_keys *const *keys, int nkeys, const uint8_
                             uint64_t n, void *const *outs, cudaStream_t st, bool v2) {
   if (!keys || !outs || nkeys < 1 || nkeys > PMP_HOST_MAX_KEYS) return PMP_EINVAL;
   for (int k = 0; k < nkeys; k++)
-    if (!keys[k] || !outs[k]) return PMP_EINVAL;
+    if (!keys[k]) return PMP_EINVAL;
+  if (n == 0) return 0;
+  for (int k = 0; k < nkeys; k++)
+    if (!outs[k]) return PMP_EINVAL;
   bool done[PMP_HOST_MAX_KEYS] = {false, false, false, false};
   // pair a 64-bit with a 32-bit schedule: one fused pass over the short strings
   for (int k = 0; k < nkeys; k++) {

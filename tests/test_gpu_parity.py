@@ -500,3 +500,35 @@ def test_random_batches_soak(torch_dev, oracle_lib, trial):
     assert np.array_equal(run_batch(torch_dev, k64, pay, off), want64)
     h64, h32 = pmp.hash_batch_host([k64, k32], pay, off, piece_bytes=int(rng.integers(1, 1 << 20)))
     assert np.array_equal(h64, want64) and np.array_equal(h32, want32)
+
+
+def test_entry_points_edge_cases(torch_dev, oracle_lib):
+    """n = 0 is a no-op and n = 1 works through every batch entry point; an
+    offsets array that is not 16-byte aligned (the kernels' TMA source) is
+    accepted; NULL arguments are PMP_EINVAL, not a fault."""
+    import torch
+
+    k64, k32 = pmp.Keys.generate(5, 64), pmp.Keys.generate(6, 32)
+    pay = datagen.payload_host(9, 0, 5000)
+    d_pay = torch.from_numpy(pay).to(torch_dev)
+    for lens in ([], [0], [1], [127], [128], [4999]):
+        off = datagen.offsets_from_lengths(np.array(lens, dtype=np.uint64)) + 1
+        d_off = torch.from_numpy(off.view(np.int64)).to(torch_dev)
+        o64, o32 = pmp.hash_batch_multi([k64, k32], d_pay, d_off)
+        h64, h32 = pmp.hash_batch_host([k64, k32], pay, off)
+        torch.cuda.synchronize()
+        if lens:
+            assert np.array_equal(pmp.as_u64(o64), oracle_batch(oracle_lib, 5, 64, pay, off))
+            assert np.array_equal(pmp.as_u64(o32), oracle_batch(oracle_lib, 6, 32, pay, off))
+            assert np.array_equal(h64, pmp.as_u64(o64)) and np.array_equal(h32, pmp.as_u64(o32))
+    # offsets starting 8 bytes into an allocation (not 16-byte aligned)
+    lens = np.arange(0, 300, dtype=np.uint64)
+    off = datagen.offsets_from_lengths(lens)
+    buf = torch.from_numpy(np.concatenate([[0], off.view(np.int64)])).to(torch_dev)
+    d_off = buf[1:]
+    assert d_off.data_ptr() % 16 == 8
+    big = torch.from_numpy(datagen.payload_host(9, 0, int(off[-1]))).to(torch_dev)
+    got = pmp.as_u64(pmp.hash_batch(k64, big, d_off))
+    assert np.array_equal(got, oracle_batch(oracle_lib, 5, 64, big.cpu().numpy(), off))
+    assert pmp.pmp_hash_batch(k64.handle, 0, d_off.data_ptr(), 3, d_off.data_ptr(), 0) == pmp.PMP_EINVAL
+    assert pmp.pmp_hash_batch_multi([k64.handle], big.data_ptr(), d_off.data_ptr(), 3, [0], 0) == pmp.PMP_EINVAL
