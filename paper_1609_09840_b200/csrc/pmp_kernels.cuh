@@ -1080,7 +1080,7 @@ constexpr size_t kWSmem = kWBlockRegion + kWBlockWarps * kWSmemPerWarp;
 
 // Mid strings in 8-lane groups (mid_phase) instead of warp per string.
 #ifndef PMP_MID_INLINE
-#define PMP_MID_INLINE __noinline__
+#define PMP_MID_INLINE __forceinline__
 #endif
 #ifndef PMP_MID_GROUPS
 #define PMP_MID_GROUPS 1
