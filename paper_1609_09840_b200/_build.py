@@ -8,7 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libpmp.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("pmp_api.cu", "pmp_kernels.cuh", "pmp_arith.cuh", "pmp_poly.cuh")] + [
+SOURCES = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh"))] + [
     os.path.join(ROOT, "include", "pmp.h")
 ]
 

@@ -1,0 +1,85 @@
+// pmp_misc.cuh -- self-test hooks and the hash-table histogram pass
+// (part of the kernels included by pmp_kernels.cuh; citations as there)
+#pragma once
+#include "pmp_common.cuh"
+
+namespace pmp {
+
+// ============================================================= self-test hooks
+// mode 0: reduce the exact value (w0 + w1 2^n + w2 2^2n) mod p through the
+//         3->2 reduction + Algorithm 2; in = 3 words, out = (lo, hi).
+// mode 1: one block f(s) = (b + sum a_i s_i) mod p with the hot-loop MAC;
+//         in = [b, a_0..a_127, s_0..s_127], out = (lo, hi).
+// mode 2: out = mix(in[0]).
+// mode 3: as mode 0 but only (value mod p) mod 2^n (the digest input).
+// Histogram of bucket ids (the hash-table consumer's counts):
+// a separate pass over the n bucket ids, privatised per block in shared memory
+// when M fits (one global atomic per non-empty bucket and block), so the
+// hashing kernels never contend on a few hundred global counters.
+constexpr uint32_t kHistSmemMax = 12288;     // counters per block (48 KB)
+__global__ void __launch_bounds__(512)
+k_histogram(const uint32_t *__restrict__ buckets, uint64_t n, uint32_t M, uint32_t *__restrict__ counts) {
+  extern __shared__ uint32_t h[];
+  const bool priv = M <= kHistSmemMax;
+  if (priv) {
+    for (uint32_t i = threadIdx.x; i < M; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+  }
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t b = __ldcs(buckets + i);
+    if (priv) atomicAdd(&h[b], 1u);
+    else atomicAdd(&counts[b], 1u);
+  }
+  if (priv) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < M; i += blockDim.x)
+      if (h[i]) atomicAdd(&counts[i], h[i]);
+  }
+}
+
+template <int BITS>
+__global__ void k_selftest(int mode, const uint64_t *__restrict__ in, uint64_t n, uint64_t *__restrict__ outv) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  if (mode == 0) {
+    const uint64_t *w = in + 3 * t;
+    if constexpr (BITS == 64) {
+      Acc5 x = {(uint32_t)w[0], (uint32_t)(w[0] >> 32), (uint32_t)w[1], (uint32_t)(w[1] >> 32), (uint32_t)w[2]};
+      fe_store(outv + 2 * t, reduce_acc5(x));
+    } else {
+      Acc3 x = {(uint32_t)w[0], (uint32_t)w[1], (uint32_t)w[2]};
+      fe_store(outv + 2 * t, reduce_acc3(x));
+    }
+  } else if (mode == 1) {
+    const uint64_t *blk = in + 257 * t;
+    if constexpr (BITS == 64) {
+      MacAcc64 A;
+      macc_zero(A);
+      for (int i = 0; i < 128; i++) mac64(A, blk[1 + i], blk[129 + i]);
+      Acc5 x = macc_normalize(A);
+      acc5_add_u64(x, blk[0]);
+      fe_store(outv + 2 * t, reduce_acc5(x));
+    } else {
+      Acc3 A = {0, 0, 0};
+      for (int i = 0; i < 128; i++) mac32(A, (uint32_t)blk[1 + i], (uint32_t)blk[129 + i]);
+      acc3_add_u64(A, blk[0]);
+      fe_store(outv + 2 * t, reduce_acc3(A));
+    }
+  } else if (mode == 3) {
+    const uint64_t *w = in + 3 * t;
+    if constexpr (BITS == 64) {
+      Acc5 x = {(uint32_t)w[0], (uint32_t)(w[0] >> 32), (uint32_t)w[1], (uint32_t)(w[1] >> 32), (uint32_t)w[2]};
+      outv[2 * t] = reduce_lo_acc5(x);
+    } else {
+      Acc3 x = {(uint32_t)w[0], (uint32_t)w[1], (uint32_t)w[2]};
+      outv[2 * t] = reduce_lo_acc3(x);
+    }
+    outv[2 * t + 1] = 0;
+  } else {
+    outv[2 * t] = BITS == 64 ? mix64(in[t]) : mix32((uint32_t)in[t]);
+    outv[2 * t + 1] = 0;
+  }
+}
+
+}  // namespace pmp

@@ -20,7 +20,7 @@
 
 namespace pmp {
 
-// (kPolyW, kPolyRP, kBlobWords and poly_pow_R live in pmp_kernels.cuh, shared
+// (kPolyW, kPolyRP, kBlobWords and poly_pow_R live in pmp_wstring.cuh, shared
 // with the batch pipeline k_wstring<BITS, true>.)
 
 // W[i] = r^(128-i), RP[k] = R^(2^k) with R = r^128 = W[0].  One thread.

@@ -1,0 +1,429 @@
+// pmp_short.cuh -- strings of <= 127 bytes: one thread per string, warp-specialised TMA pipeline (k_short)
+// (part of the kernels included by pmp_kernels.cuh; citations as there)
+#pragma once
+#include "pmp_common.cuh"
+
+namespace pmp {
+
+// ============================================================= k_short
+// One short string (B <= kShortMax, so T = floor(B/w)+1 <= 16 / 32 words and
+// the tree is a single f_1 block, or no block at all when T == 1).
+// fetch(k) returns the k-th aligned 32-bit word of the region starting at the
+// word containing the string's first byte; `sh` is that byte's bit offset.
+// The loop runs to the warp's largest number of full words; a lane past its
+// own full words multiplies zeros (a*0 adds nothing), so the multiply-adds are
+// never branched around.  The marker word is done once per lane with
+// its key read from shared memory.
+// V2: the two-level variant (reading Q19): V = b_2 + r * v_0 with v_0 = f_1 of
+// the single chunk (no |sigma| = 1 shortcut).
+template <int BITS, bool V2, class Fetch>
+PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ skeys, uint32_t B, uint32_t sh,
+                              int tfull_max, Fetch fetch) {
+  if constexpr (BITS == 64) {
+    const int tlast = (int)(B >> 3);
+    const uint32_t r = B & 7;
+    MacAcc64 A;
+    macc_zero(A);
+    uint32_t y0 = fetch(0);
+#pragma unroll
+    for (int tb = 0; tb < 16; tb += kShortG64) {
+      if (tb >= tfull_max) break;                              // warp-uniform, once per kShortG64 words
+#pragma unroll
+      for (int j = 0; j < kShortG64; j++) {
+        const int t = tb + j;
+        if (t >= 15) break;                                    // compile-time
+        const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
+        uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
+        y0 = y2;
+        if ((uint32_t)t >= (uint32_t)tlast) lo = hi = 0;       // past this lane's full words
+        mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lo, hi);  // Eq. (1), lazy
+      }
+    }
+    const uint32_t z0 = fetch(2 * tlast), z1 = fetch(2 * tlast + 1), z2 = fetch(2 * tlast + 2);
+    const uint32_t zl = funnel(z0, z1, sh), zh = funnel(z1, z2, sh);
+    // bytes || 0x01 || 0: mask the half holding byte r, keep / drop the other
+    const uint32_t mb = 1u << (8 * (r & 3)), wh = (((r & 4) ? zh : zl) & (mb - 1)) | mb;
+    const uint64_t w = (r & 4) ? ((uint64_t)wh << 32) | zl : (uint64_t)wh;
+    if (!V2 && tlast == 0) return w;                           // |sigma| = 1: no f_j (reading Q2)
+    mac64(A, skeys[tlast], w);
+    Acc5 x = macc_normalize(A);
+    acc5_add_u64(x, K.b);
+    if constexpr (V2) {
+      const Fe64 v0 = reduce_acc5(x);
+      Acc5 y = {0, 0, 0, 0, 0};
+      acc5_mac_fe(y, K.r, v0);
+      acc5_add_u64(y, K.b2);
+      return reduce_lo_acc5(y);
+    }
+    return reduce_lo_acc5(x);                                  // mod p, then mod 2^64
+  } else {
+    const int tlast = (int)(B >> 2);
+    const uint32_t r = B & 3;
+    Acc3 A = {0, 0, 0};
+    uint32_t y0 = fetch(0);
+#pragma unroll
+    for (int tb = 0; tb < 32; tb += kShortG32) {
+      if (tb >= tfull_max) break;                              // warp-uniform, once per kShortG32 words
+#pragma unroll
+      for (int j = 0; j < kShortG32; j++) {
+        const int t = tb + j;
+        if (t >= 31) break;
+        const uint32_t y1 = fetch(t + 1);
+        uint32_t w = funnel(y0, y1, sh);
+        y0 = y1;
+        if ((uint32_t)t >= (uint32_t)tlast) w = 0;
+        mac32(A, (uint32_t)K.a[t], w);
+      }
+    }
+    const uint32_t z0 = fetch(tlast), z1 = fetch(tlast + 1);
+    uint32_t w = funnel(z0, z1, sh);
+    w = (w & ((1u << (8 * r)) - 1)) | (1u << (8 * r));
+    if (!V2 && tlast == 0) return w;
+    mac32(A, (uint32_t)skeys[tlast], w);
+    acc3_add_u64(A, K.b);
+    if constexpr (V2) {
+      const uint64_t v0 = reduce_acc3(A);
+      Acc3 y = {0, 0, 0};
+      acc3_mac_fe(y, (uint32_t)K.r, v0);
+      acc3_add_u64(y, K.b2);
+      return reduce_lo_acc3(y);
+    }
+    return reduce_lo_acc3(A);
+  }
+}
+
+// Both digests of one short string in one pass (a 64-bit and a 32-bit key
+// schedule: the two configs[1] outputs).  The 32-bit words of PM+32 are the
+// halves of the 64-bit words of PM+64, so the loads, funnel shifts, masks and
+// the loop over the full 64-bit words (warp maximum tfull_max) are shared;
+// each width keeps its own marker word, exact sum and reduction.
+// V2: the two-level variant (reading Q19) for both schedules: V = b_2 + r v_0,
+// every string (no |sigma| = 1 shortcut).
+template <bool V2, class Fetch>
+PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ skeys, const uint32_t *__restrict__ skeys32,
+                            uint32_t B, uint32_t sh, int tfull_max, Fetch fetch, uint64_t &lo64, uint32_t &lo32) {
+  const int tl64 = (int)(B >> 3), tl32 = (int)(B >> 2);
+  MacAcc64 A;
+  macc_zero(A);
+  Acc3 C = {0, 0, 0};
+  uint32_t y0 = fetch(0);
+#pragma unroll
+  for (int tb = 0; tb < 16; tb += kShortG64) {
+    if (tb >= tfull_max) break;                              // warp-uniform
+#pragma unroll
+    for (int j = 0; j < kShortG64; j++) {
+      const int t = tb + j;
+      if (t >= 16) break;                                    // compile-time
+      const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
+      const uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
+      y0 = y2;
+      // both halves of a full 64-bit word are full PM+32 words; the one PM+32
+      // word beyond them (the low half at t = tl64 when B mod 8 >= 4) is added
+      // with the markers below
+      const bool f64 = t < tl64;
+      const uint32_t lm = f64 ? lo : 0u, hm = f64 ? hi : 0u;
+      if (t < 15) {
+        mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lm, hm);  // Eq. (1)
+        mac32(C, K.a32[2 * t], lm);
+        mac32(C, K.a32[2 * t + 1], hm);
+      }
+    }
+  }
+  // marker words: the 8 bytes at 8 tl64, and its half holding byte 4 tl32
+  const uint32_t z0 = fetch(2 * tl64), z1 = fetch(2 * tl64 + 1), z2 = fetch(2 * tl64 + 2);
+  const uint32_t zl = funnel(z0, z1, sh), zh = funnel(z1, z2, sh);
+  // the partial 32-bit word is the PM+32 marker word, and a half of the PM+64 one
+  const bool up = (B & 4) != 0;                              // B mod 8 >= 4
+  const uint32_t mb = 1u << (8 * (B & 3));
+  const uint32_t w32 = ((up ? zh : zl) & (mb - 1)) | mb;
+  const uint64_t w = up ? ((uint64_t)w32 << 32) | zl : (uint64_t)w32;
+  if (up) mac32(C, skeys32[2 * tl64], zl);                   // the full PM+32 word 2 tl64
+  if (!V2 && tl64 == 0) {
+    lo64 = w;                                                // |sigma| = 1 (reading Q2)
+  } else {
+    mac64(A, skeys[tl64], w);
+    Acc5 x = macc_normalize(A);
+    acc5_add_u64(x, K.b);
+    if constexpr (V2) {
+      const Fe64 v0 = reduce_acc5(x);
+      Acc5 y = {0, 0, 0, 0, 0};
+      acc5_mac_fe(y, K.r, v0);
+      acc5_add_u64(y, K.b2);
+      lo64 = reduce_lo_acc5(y);
+    } else {
+      lo64 = reduce_lo_acc5(x);
+    }
+  }
+  if (!V2 && tl32 == 0) {
+    lo32 = w32;
+  } else {
+    mac32(C, skeys32[tl32], w32);
+    acc3_add_u64(C, K.b32);
+    if constexpr (V2) {
+      const uint64_t v0 = reduce_acc3(C);
+      Acc3 y = {0, 0, 0};
+      acc3_mac_fe(y, (uint32_t)K.r32, v0);
+      acc3_add_u64(y, K.b2_32);
+      lo32 = reduce_lo_acc3(y);
+    } else {
+      lo32 = reduce_lo_acc3(C);
+    }
+  }
+}
+
+// k_short: warp-specialised TMA pipeline.  A block = 1 producer warp + kShortWarps
+// consumer warps, working on tiles of kTile = 32 * kShortWarps consecutive
+// strings (grid-strided).  Shared memory holds
+//   - an offsets ring (kRing slots): the kTile+1 offsets of tile k, one TMA bulk
+//     copy issued kOffAhead tiles ahead;
+//   - a byte ring (kByteRing bytes): the 16-byte aligned contiguous byte span of
+//     each staged tile, one TMA bulk copy, packed back to back so the number of
+//     tiles in flight adapts to the string lengths;
+//   - a header per tile.
+// The producer's work per tile is O(1) (the span is [offsets[first],
+// offsets[last+1])), so one producer warp keeps many consumer warps fed.  A
+// tile whose span exceeds kSpanMaxTile is "direct": consumers read its short
+// strings from global.  Strings longer than kShortMax are appended by the
+// consumers to the work list of k_wstring in either mode.
+constexpr int kPasses = 1;                                     // strings per consumer lane per tile
+constexpr int kTile = 32 * kShortWarps * kPasses;              // 384
+#ifndef PMP_SHORT_SLOTS
+#define PMP_SHORT_SLOTS 8
+#endif
+constexpr int kRing = PMP_SHORT_SLOTS, kOffAhead = PMP_SHORT_SLOTS / 2;  // tile slots (power of 2), offsets prefetch
+constexpr uint32_t kByteRing = PMP_SHORT_RING_KB * 1024;
+// Block-wide counting sort of each tile by word count before hashing
+// (PMP_SHORT_SORT=1): removes most of the zero-padding multiply-adds but costs
+// two named barriers per tile; measured 4-10% slower on configs[1]
+// (profiles/r01_summary.md), so it is off.
+#ifndef PMP_SHORT_SORT
+#define PMP_SHORT_SORT 0
+#endif
+constexpr uint32_t kSpanMaxTile = kByteRing / 2 < 32 * 1024 ? kByteRing / 2 : 32 * 1024;  // larger spans go direct
+constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
+constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
+struct TileHdr {
+  uint64_t alo;    // global address of staged byte 0
+  uint32_t pos;    // ring position of staged byte 0
+  uint32_t mode;   // 0 staged, 1 direct
+};
+constexpr size_t kShortSmem = 384 /* keys */ + kByteRing + kSlack + 16 + (size_t)kRing * kOffBytes +
+                              (size_t)kRing * sizeof(TileHdr) +
+                              (size_t)(3 * kRing) * 8 + (PMP_SHORT_SORT ? 256 /* sort histograms */ + 2 * kTile /* permutation */ : 0) + 128;
+
+// DUAL: BITS = 64 and a second, 32-bit schedule in K.a32 / K.b32 whose digests go to os2
+template <int BITS, bool V2 = false, bool DUAL = false>
+__global__ void __launch_bounds__((kShortWarps + 1) * 32)
+k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets,
+        uint64_t n, const OutSpec os, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount,
+        const OutSpec os2) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint64_t *skeys = reinterpret_cast<uint64_t *>(smem);                       // a_{1,0..31}
+  uint32_t *skeys32 = reinterpret_cast<uint32_t *>(smem + 256);               // DUAL: 32-bit a_{1,0..31}
+  uint8_t *ring = smem + 384;                                                  // kByteRing (+ slack)
+  uint64_t *offs = reinterpret_cast<uint64_t *>(ring + kByteRing + kSlack + 16);  // kRing x kOffBytes
+  TileHdr *hdr = reinterpret_cast<TileHdr *>(reinterpret_cast<uint8_t *>(offs) + (size_t)kRing * kOffBytes);
+  uint64_t *bar_off = reinterpret_cast<uint64_t *>(hdr + kRing);  // offsets landed (producer)
+  uint64_t *bar_done = bar_off + kRing;                            // tile consumed (producer)
+  uint64_t *bar_full = bar_done + kRing;                           // tile ready (consumers)
+  if (threadIdx.x < 32) skeys[threadIdx.x] = K.a[threadIdx.x];
+  if (DUAL && threadIdx.x < 32) skeys32[threadIdx.x] = K.a32[threadIdx.x];
+#if PMP_SHORT_SORT
+  uint32_t *s_hist = reinterpret_cast<uint32_t *>(bar_full + kRing);  // 2 x 32 class counters
+  uint16_t *s_perm = reinterpret_cast<uint16_t *>(s_hist + 64);      // kTile sorted slots
+  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
+#endif
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kRing; q++) {
+      mbar_init(&bar_off[q], 1);
+      mbar_init(&bar_done[q], kShortWarps);
+      mbar_init(&bar_full[q], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const uint32_t ntiles = (uint32_t)((n + kTile - 1) / kTile);
+  // tiles of this block: blockIdx.x + k * gridDim.x
+  const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto tile_base = [&](uint32_t k) { return ((uint64_t)blockIdx.x + (uint64_t)k * gridDim.x) * kTile; };
+  auto off_slot = [&](uint32_t k) { return offs + (size_t)(k & (kRing - 1)) * (kOffBytes / 8); };
+
+  if (wib == kShortWarps) {
+    // ------------------------------------------------------------ producer warp
+    auto wait_done = [&](uint32_t k) {  // tile k fully consumed
+      mbar_wait(&bar_done[k & (kRing - 1)], (k / kRing) & 1);
+    };
+    auto issue_offs = [&](uint32_t k) {
+      if (k >= kRing) wait_done(k - kRing);  // slot reuse
+      if (lane == 0) {
+        const int q = (int)(k & (kRing - 1));
+        const uint64_t base = tile_base(k);
+        const uint64_t cnt = min((uint64_t)kTile + 1, n + 1 - base);
+        const uint32_t nb = (uint32_t)((cnt * 8 + 15) & ~15ULL);
+        mbar_arrive_tx(&bar_off[q], nb);
+        bulk_g2s(off_slot(k), offsets + base, nb, &bar_off[q]);
+      }
+    };
+    // byte-ring bookkeeping (identical in every lane): [tail, head) is in use;
+    // tile k's bytes end at tend[k % kRing]; `oldest` is the first unreleased tile.
+    uint32_t head = 0, tail = 0, oldest = 0;
+    __shared__ uint32_t tend[kRing];
+    for (uint32_t k = 0; k < (uint32_t)kOffAhead && k < my_tiles; k++) issue_offs(k);
+    for (uint32_t k = 0; k < my_tiles; k++) {
+      const int q = (int)(k & (kRing - 1));
+      if (k + kOffAhead < my_tiles) issue_offs(k + kOffAhead);
+      mbar_wait(&bar_off[q], (k / kRing) & 1);
+      const uint64_t base = tile_base(k);
+      const uint32_t nv = (uint32_t)min((uint64_t)kTile, n - base);  // strings in this tile
+      const uint64_t *o = off_slot(k);
+      // span of the tile and its place in the byte ring
+      uint32_t mode = 1, nb = 0, pos = 0;
+      uintptr_t alo = 0;
+      {
+        const uint64_t first = o[0], endo = o[nv];
+        alo = (uintptr_t)(bytes + first) & ~(uintptr_t)15;
+        const uintptr_t ahi = ((uintptr_t)(bytes + endo) + 15) & ~(uintptr_t)15;
+        const uint64_t span = first < endo ? (uint64_t)(ahi - alo) : 0;
+        if (span <= kSpanMaxTile) {
+          mode = 0;
+          nb = (uint32_t)span;
+          uint32_t start = head;
+          if ((start % kByteRing) + nb > kByteRing) start += kByteRing - (start % kByteRing);  // no wrap inside a span
+          while (start + nb - tail > kByteRing) {  // release consumed tiles until the span fits
+            wait_done(oldest);
+            tail = tend[oldest & (kRing - 1)];
+            oldest++;
+          }
+          pos = start % kByteRing;
+          head = start + nb;
+        }
+      }
+      // keep `oldest` within kRing of k so tend[] slots are not overwritten early
+      while (k - oldest >= (uint32_t)kRing - 1) {
+        wait_done(oldest);
+        tail = tend[oldest & (kRing - 1)];
+        oldest++;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        tend[q] = head;
+        hdr[q].alo = (uint64_t)alo;
+        hdr[q].pos = pos;
+        hdr[q].mode = mode;
+        mbar_arrive_tx(&bar_full[q], nb);   // release: hdr and offsets visible to consumers
+        if (nb) bulk_g2s(ring + pos, reinterpret_cast<const void *>(alo), nb, &bar_full[q]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumer warps
+  // shared-window addresses computed once (the loop uses explicit ld.shared)
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t offs_s = smem_u32(offs) + 8u * (32u * wib + lane);
+  const uint32_t hdr_s = smem_u32(hdr), full_s = smem_u32(bar_full), done_s = smem_u32(bar_done);
+  const uint64_t tstride = (uint64_t)gridDim.x * kTile;
+  const uint32_t ct = 32u * wib + lane;                 // consumer thread = string slot in the tile
+#if PMP_SHORT_SORT
+  const uint32_t offs0_s = smem_u32(offs), hist_s = smem_u32(s_hist), perm_s = smem_u32(s_perm);
+#endif
+  uint64_t ibase = (uint64_t)blockIdx.x * kTile;
+  for (uint32_t k = 0; k < my_tiles; k++, ibase += tstride) {
+    const uint32_t q = k & (kRing - 1);
+    uint64_t i = ibase + ct;
+    mbar_wait_s(full_s + 8 * q, (k / kRing) & 1);
+    uint64_t ralo;
+    uint32_t rpos, mode;
+    lds_hdr(hdr_s + 16 * q, ralo, rpos, mode);
+    bool valid = i < n;
+    uint64_t o0, o1;
+    lds_u64x2(offs_s + q * kOffBytes, o0, o1);      // offsets[i], offsets[i+1] (slot-local)
+    const uint64_t Bl = valid ? o1 - o0 : 0;
+    bool is_short = Bl <= kShortMax;                 // invalid lanes: an empty string, not stored
+    const bool is_long = !is_short;
+    uint32_t B = (uint32_t)Bl;
+    const unsigned longmask = __ballot_sync(FULL, is_long);
+    if (longmask) {
+      // warp-aggregated append: big strings from the back, others from the front
+      const bool big = is_long && Bl >= kBigBytes;
+      const unsigned bigmask = __ballot_sync(FULL, big), midmask = longmask & ~bigmask;
+      uint32_t mbase = 0, bbase = 0;
+      if (lane == 0) {
+        if (midmask) mbase = atomicAdd(&wcount[0], (uint32_t)__popc(midmask));
+        if (bigmask) bbase = atomicAdd(&wcount[1], (uint32_t)__popc(bigmask));
+      }
+      mbase = __shfl_sync(FULL, mbase, 0);
+      bbase = __shfl_sync(FULL, bbase, 0);
+      const unsigned lt = (1u << lane) - 1;
+      if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
+      if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
+    }
+#if PMP_SHORT_SORT
+    // ---- counting sort of the tile's strings by word count (block-wide, two
+    // named barriers): warp w then hashes sorted strings 32w..32w+31, whose
+    // word counts differ by at most one class, so the word loop below runs
+    // to (almost) every lane's own length instead of the longest string of
+    // 32 random ones.  Long / past-n strings sort last and are skipped.
+    {
+      const uint32_t cls = is_short ? min(B / (uint32_t)(BITS / 8), 30u) : 31u;
+      const uint32_t hb = hist_s + 128u * (k & 1);
+      const uint32_t rank = atoms_add(hb + 4 * cls, 1u);
+      named_bar_sync(1, kShortWarps * 32);
+      const uint32_t h = lds_u32(hb + 4 * lane);
+      uint32_t incl = h;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const uint32_t start = __shfl_sync(FULL, incl - h, (int)cls);
+      sts_u16(perm_s + 2 * (start + rank), (uint16_t)ct);
+      named_bar_sync(1, kShortWarps * 32);
+      if (ct < 32) sts_u32(hb + 4 * ct, 0u);
+      const uint32_t j = lds_u16(perm_s + 2 * ct);
+      uint64_t p0, p1;
+      lds_u64x2(offs0_s + q * kOffBytes + 8 * j, p0, p1);
+      i = ibase + j;
+      valid = i < n;
+      o0 = p0;
+      const uint64_t Bj = valid ? p1 - p0 : 0;
+      is_short = Bj <= kShortMax;
+      B = (uint32_t)Bj;
+    }
+#endif
+    // warp max of the number of full words (the marker word is handled apart)
+    const int tfm = (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
+    if (is_short) {
+      uint64_t lo;
+      uint32_t lo32 = 0;
+      if (mode == 0) {
+        // (lanes past n read the tile's first bytes: in bounds, result not stored)
+        const uint32_t sofs = rpos + (valid ? (uint32_t)((uintptr_t)(bytes + o0) - (uintptr_t)ralo) : 0u);
+        const uint32_t pa = ring_s + (sofs & ~3u);
+        auto fetch = [&](int kk) { return lds_u32(pa + 4 * kk); };
+        if constexpr (DUAL) short_tree_dual<V2>(K, skeys, skeys32, B, 8 * (sofs & 3), tfm, fetch, lo, lo32);
+        else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (sofs & 3), tfm, fetch);
+      } else {
+        // direct tile: read the string's aligned 32-bit words straight from global,
+        // touching only words that overlap [start, end) (never past offsets[n]).
+        const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
+        const uintptr_t pa = sa & ~(uintptr_t)3;
+        auto fetch = [&](int kk) {
+          const uintptr_t a = pa + 4 * (uintptr_t)kk;
+          return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
+        };
+        if constexpr (DUAL) short_tree_dual<V2>(K, skeys, skeys32, B, 8 * (uint32_t)(sa & 3), tfm, fetch, lo, lo32);
+        else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, fetch);
+      }
+      if (valid) {
+        emit<BITS>(os, i, lo);
+        if constexpr (DUAL) emit<32>(os2, i, lo32);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_s(done_s + 8 * q);
+  }
+}
+
+}  // namespace pmp
