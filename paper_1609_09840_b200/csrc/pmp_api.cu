@@ -671,11 +671,11 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     return PMP_EINVAL;
   const int sms = sm_count(k->device);
   Scratch sc(st), sc_off(st);
-  // work list (n u32) + counters [mid, big, next big, next mid batch]
-  if (sc.alloc((size_t)n * 4 + 16)) return PMP_ENOMEM;
+  // work list (n u32) + counters [mid, big, then per schedule: next big, next mid batch]
+  if (sc.alloc((size_t)n * 4 + 32)) return PMP_ENOMEM;
   uint32_t *wcount = (uint32_t *)sc.p;
-  uint32_t *wlist = wcount + 4;
-  if (cudaMemsetAsync(wcount, 0, 16, st) != cudaSuccess) return PMP_ECUDA;
+  uint32_t *wlist = wcount + 8;
+  if (cudaMemsetAsync(wcount, 0, 24, st) != cudaSuccess) return PMP_ECUDA;
   ParamKeys pk = param_keys(k);
   if (dual) {
     for (int i = 0; i < 32; i++) pk.a32[i] = (uint32_t)k2->a[i];
@@ -692,8 +692,9 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     }
-    const void *ws[4] = {(const void *)k_wstring<64>, (const void *)k_wstring<32>, (const void *)k_wstring<64, true>,
-                         (const void *)k_wstring<32, true>};
+    const void *ws[6] = {(const void *)k_wstring<64>, (const void *)k_wstring<32>, (const void *)k_wstring<64, true>,
+                         (const void *)k_wstring<32, true>, (const void *)k_wstring_dual<false>,
+                         (const void *)k_wstring_dual<true>};
     for (const void *f : ws) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
   });
   // the offsets ring is fed by TMA bulk copies, which need 16-byte aligned sources
@@ -733,11 +734,17 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
       cudaLaunchKernel(kw, dim3(wgrid), dim3(kWBlockWarps * 32), args, kWSmem, st);
     });
   };
-  rc = launch_w(k, os);
-  if (rc || !dual) return rc;
-  // second schedule over the same work list: reset the claim counters
-  if (cudaMemsetAsync(wcount + 2, 0, 8, st) != cudaSuccess) return PMP_ECUDA;
-  return launch_w(k2, *os2);
+  if (!dual) return launch_w(k, os);
+  // both schedules over the shared work list in one launch (half the blocks each)
+  const void *kw = v2 ? (const void *)k_wstring_dual<true> : (const void *)k_wstring_dual<false>;
+  const unsigned wgrid = (unsigned)(2 * ((sms * resident_blocks(kw, kWBlockWarps * 32, kWSmem, "k_wstring") + 1) / 2));
+  const uint64_t *b64 = k->d_blob, *b32 = k2->d_blob;
+  const OutSpec o32 = *os2;
+  return launch("k_wstring", st, [&] {
+    void *args[] = {(void *)&b64, (void *)&b32, (void *)&bytes, (void *)&offsets, (void *)&n, (void *)&os,
+                    (void *)&o32, (void *)&wlist, (void *)&wcount};
+    cudaLaunchKernel(kw, dim3(wgrid), dim3(kWBlockWarps * 32), args, kWSmem, st);
+  });
 }
 
 int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,

@@ -128,7 +128,7 @@ constexpr size_t kMSmemPerWarp = ((size_t)kMStages * (4 * kMSlot + 4 * sizeof(MH
 template <int BITS, bool POLY>
 __device__ PMP_MID_INLINE void mid_phase(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
                                        const uint64_t *__restrict__ offsets, const OutSpec &os,
-                                       const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount,
+                                       const uint32_t *__restrict__ wlist, uint32_t *__restrict__ claims,
                                        uint32_t nmid, const uint64_t *s_a2, const uint64_t *s_mklo,
                                        const uint32_t *s_mkhi, const uint64_t *s_a1, uint64_t b1, uint64_t b2,
                                        typename Tr<BITS>::Fe v1mk, uint8_t *wbase) {
@@ -156,7 +156,7 @@ __device__ PMP_MID_INLINE void mid_phase(const uint64_t *__restrict__ keys, cons
   uint64_t cur_o0 = 0, cur_o1 = 0, nxt_o0 = 0, nxt_o1 = 0;
   auto fetch_batch = [&]() {  // -> nxt
     uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(&wcount[3], 32u);
+    if (lane == 0) base = atomicAdd(&claims[1], 32u);
     base = __shfl_sync(FULL, base, 0);
     nxt_n = base < nmid ? min(32u, nmid - base) : 0u;
     if ((uint32_t)lane < nxt_n) {
@@ -403,11 +403,14 @@ __device__ PMP_MID_INLINE void mid_phase(const uint64_t *__restrict__ keys, cons
 #ifndef PMP_W_MINB
 #define PMP_W_MINB 5
 #endif
-template <int BITS, bool POLY = false>
-__global__ void __launch_bounds__(kWBlockWarps * 32, PMP_W_MINB)
-k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
-          const uint64_t *__restrict__ offsets, uint64_t n, const OutSpec os,
-          const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
+// The kernel body over blocks bid = 0 .. nblocks-1 of its launch; work counts
+// in wcount[0..1] (mid, big), claim counters in claims[0..1] (next big string,
+// next mid batch) -- one pair per key schedule when two share a launch.
+template <int BITS, bool POLY>
+__device__ __forceinline__ void wstring_body(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
+                                             const uint64_t *__restrict__ offsets, uint64_t n, const OutSpec &os,
+                                             const uint32_t *__restrict__ wlist, const uint32_t *__restrict__ wcount,
+                                             uint32_t *__restrict__ claims, uint32_t bid, uint32_t nblocks) {
   using T = Tr<BITS>;
   using Acc = typename T::Acc;
   using Fe = typename T::Fe;
@@ -485,7 +488,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   };
 
   // ---- work-item source (warp-uniform state) ----
-  const uint32_t gw = blockIdx.x * kWBlockWarps + wib, nw = gridDim.x * kWBlockWarps;
+  const uint32_t gw = bid * kWBlockWarps + wib, nw = nblocks * kWBlockWarps;
   // big strings: claim pipeline.  cl = 0 idle/exhausted, 1 atomic issued (lane 0),
   // 2 work-list entry loading, 3 offsets loading; each step consumes the
   // previous step's load, so it only stalls if that load is still in flight.
@@ -509,7 +512,7 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
     }
   };
   auto claim_start = [&]() {
-    if (lane == 0) cl_item = atomicAdd(&wcount[2], 1u);
+    if (lane == 0) cl_item = atomicAdd(&claims[0], 1u);
     cl = 1;
   };
   if (big_open) claim_start();
@@ -870,9 +873,36 @@ k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
   if (lane == 0)   // the big phase's barriers sit in memory mid_phase reuses
     for (int q = 0; q < kWStages; q++) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar[q])) : "memory");
   __syncwarp();
-  mid_phase<BITS, POLY>(keys, bytes, offsets, os, wlist, wcount, nmid, s_a2, s_mklo, s_mkhi, s_a1, b1, b2,
+  mid_phase<BITS, POLY>(keys, bytes, offsets, os, wlist, claims, nmid, s_a2, s_mklo, s_mkhi, s_a1, b1, b2,
                         v1mk, wbase);
 #endif
+}
+
+template <int BITS, bool POLY = false>
+__global__ void __launch_bounds__(kWBlockWarps * 32, PMP_W_MINB)
+k_wstring(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ bytes,
+          const uint64_t *__restrict__ offsets, uint64_t n, const OutSpec os,
+          const uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount) {
+  wstring_body<BITS, POLY>(keys, bytes, offsets, n, os, wlist, wcount, wcount + 2, blockIdx.x, gridDim.x);
+}
+
+// Both schedules of a fused two-width pass in one launch over the shared work
+// list: the first half of the blocks hashes it under the 64-bit schedule, the
+// second half under the 32-bit one (own claim counters wcount[2..3], [4..5]).
+// One launch instead of two (an empty k_wstring launch costs ~6 us, as much as
+// 2% of the configs[1] step).
+template <bool POLY = false>
+__global__ void __launch_bounds__(kWBlockWarps * 32, PMP_W_MINB)
+k_wstring_dual(const uint64_t *__restrict__ keys64, const uint64_t *__restrict__ keys32,
+               const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets, uint64_t n,
+               const OutSpec os64, const OutSpec os32, const uint32_t *__restrict__ wlist,
+               uint32_t *__restrict__ wcount) {
+  const uint32_t half = gridDim.x / 2;
+  if (blockIdx.x < half)
+    wstring_body<64, POLY>(keys64, bytes, offsets, n, os64, wlist, wcount, wcount + 2, blockIdx.x, half);
+  else
+    wstring_body<32, POLY>(keys32, bytes, offsets, n, os32, wlist, wcount, wcount + 4, blockIdx.x - half,
+                           gridDim.x - half);
 }
 
 }  // namespace pmp
