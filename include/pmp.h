@@ -241,7 +241,9 @@ int pmp_long_constant(const pmp_keys *keys, uint64_t total_len, uint64_t *c2);
  *         hot-loop multiply-accumulate;
  * mode 2: in = n words -> mix_n(word);
  * mode 3: as mode 0 but returns only (value mod p) mod 2^n, the folded
- *         form the digest path uses.
+ *         form the digest path uses;
+ * mode 4: as mode 0 by the folded reduction returning the full residue
+ *         (PM+64; PM+32 as mode 0), used by the two-level short strings.
  * in/out (device); out gets 2 uint64 per record (lo, hi). */
 int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_t *out,
                  struct CUstream_st *stream);

@@ -992,7 +992,7 @@ int pmp_long_constant(const pmp_keys *k, uint64_t total, uint64_t *c2) {
 }
 
 int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_t *out, cudaStream_t st) {
-  if ((out_bits != 32 && out_bits != 64) || mode < 0 || mode > 3 || (n && (!in || !out))) return PMP_EINVAL;
+  if ((out_bits != 32 && out_bits != 64) || mode < 0 || mode > 4 || (n && (!in || !out))) return PMP_EINVAL;
   if (n == 0) return 0;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return PMP_ENODEV;

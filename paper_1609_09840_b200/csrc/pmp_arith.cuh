@@ -243,6 +243,29 @@ PMP_HDI uint64_t reduce_lo_words64(uint64_t w0, uint64_t w1, uint64_t w2) {
   const uint64_t kv = kK64 * y1;
   return y0 - kv + (y0 < kv ? kK64 : 0);
 }
+// The same folding, returning the canonical residue V = S mod p (lo, hi):
+// V = y0 - k y1 when y0 >= k y1; otherwise V = y0 - k y1 + k + 2^64, which is
+// >= 2^64 (hi = 1) exactly when y0 + k >= k y1.  Used where the full value
+// feeds another multiply (the two-level variant's short strings).
+PMP_HDI Fe64 reduce_fe_words64(uint64_t w0, uint64_t w1, uint64_t w2) {
+  const uint32_t K = (uint32_t)w2 * (uint32_t)(kK64 * kK64) + (uint32_t)(kK64 * kK64 + kK64);
+  const uint64_t A = (uint64_t)(~(uint32_t)w1) * kK64 + K;
+  const uint64_t Bm = (uint64_t)(~(uint32_t)(w1 >> 32)) * kK64;
+  uint64_t y0 = w0 + A;
+  uint32_t y1 = y0 < A;
+  const uint64_t bs = Bm << 32;
+  y0 += bs;
+  y1 += (uint32_t)(y0 < bs) + (uint32_t)(Bm >> 32);
+  const uint64_t kv = kK64 * y1;
+  const bool neg = y0 < kv;
+  Fe64 v;
+  v.lo = y0 - kv + (neg ? kK64 : 0);
+  v.hi = neg && (y0 + kK64 >= kv);
+  return v;
+}
+PMP_HDI Fe64 reduce_fe_acc5(const Acc5 &x) {
+  return reduce_fe_words64(((uint64_t)x.c1 << 32) | x.c0, ((uint64_t)x.c3 << 32) | x.c2, x.c4);
+}
 PMP_HDI uint64_t reduce_lo_acc5(const Acc5 &x) {
   return reduce_lo_words64(((uint64_t)x.c1 << 32) | x.c0, ((uint64_t)x.c3 << 32) | x.c2, x.c4);
 }

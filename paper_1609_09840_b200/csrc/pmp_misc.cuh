@@ -66,6 +66,15 @@ __global__ void k_selftest(int mode, const uint64_t *__restrict__ in, uint64_t n
       acc3_add_u64(A, blk[0]);
       fe_store(outv + 2 * t, reduce_acc3(A));
     }
+  } else if (mode == 4) {
+    const uint64_t *w = in + 3 * t;
+    if constexpr (BITS == 64) {
+      Acc5 x = {(uint32_t)w[0], (uint32_t)(w[0] >> 32), (uint32_t)w[1], (uint32_t)(w[1] >> 32), (uint32_t)w[2]};
+      fe_store(outv + 2 * t, reduce_fe_acc5(x));
+    } else {
+      Acc3 x = {(uint32_t)w[0], (uint32_t)w[1], (uint32_t)w[2]};
+      fe_store(outv + 2 * t, reduce_acc3(x));
+    }
   } else if (mode == 3) {
     const uint64_t *w = in + 3 * t;
     if constexpr (BITS == 64) {

@@ -49,7 +49,7 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
     Acc5 x = macc_normalize(A);
     acc5_add_u64(x, K.b);
     if constexpr (V2) {
-      const Fe64 v0 = reduce_acc5(x);
+      const Fe64 v0 = reduce_fe_acc5(x);
       Acc5 y = {0, 0, 0, 0, 0};
       acc5_mac_fe(y, K.r, v0);
       acc5_add_u64(y, K.b2);
@@ -145,7 +145,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
     Acc5 x = macc_normalize(A);
     acc5_add_u64(x, K.b);
     if constexpr (V2) {
-      const Fe64 v0 = reduce_acc5(x);
+      const Fe64 v0 = reduce_fe_acc5(x);
       Acc5 y = {0, 0, 0, 0, 0};
       acc5_mac_fe(y, K.r, v0);
       acc5_add_u64(y, K.b2);

@@ -73,17 +73,19 @@ def test_reduction_fuzz_and_algorithm2_branches(torch_dev, oracle_lib, bits):
     arr = np.array(cases, dtype=np.uint64)
     d_in = torch.from_numpy(arr.view(np.int64)).to(torch_dev)
     outs = {}
-    for mode in (0, 3):  # full canonical residue; folded V mod 2^n used by the digest path
+    for mode in (0, 3, 4):  # full residue (Alg. 2); folded V mod 2^n (digests); folded full residue
         d_out = torch.zeros(2 * len(cases), dtype=torch.int64, device=torch_dev)
         rc = pmp.pmp_selftest(bits, mode, d_in.data_ptr(), len(cases), d_out.data_ptr(),
                               torch.cuda.current_stream().cuda_stream)
         assert rc == 0
         outs[mode] = d_out.cpu().numpy().view(np.uint64).reshape(-1, 2)
-    for (w0, w1, w2), (lo, hi), (lo3, _) in zip(cases, outs[0], outs[3]):
+    for (w0, w1, w2), (lo, hi), (lo3, _), (lo4, hi4) in zip(cases, outs[0], outs[3], outs[4]):
         val = int(w0) + (int(w1) << n_bits) + (int(w2) << (2 * n_bits))
         got = int(lo) + (int(hi) << 64) if bits == 64 else int(lo)
         assert got == val % p, (w0, w1, w2)
         assert int(lo3) == (val % p) & mask, (w0, w1, w2)
+        got4 = int(lo4) + (int(hi4) << 64) if bits == 64 else int(lo4)
+        assert got4 == val % p, (w0, w1, w2)
 
 
 @pytest.mark.parametrize("bits", [32, 64])
