@@ -107,11 +107,15 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   macc_zero(A);
   Acc3 C = {0, 0, 0};
   uint32_t y0 = fetch(0);
+  // exit test granularity: the warp maximum is 7 or 8 full words for configs[1],
+  // so the tree pass tests once per 8 words (measured +0.9%; the two-level pass
+  // and the single-width kernels are faster with 4)
+  constexpr int G = V2 ? kShortG64 : 8;
 #pragma unroll
-  for (int tb = 0; tb < 16; tb += kShortG64) {
+  for (int tb = 0; tb < 16; tb += G) {
     if (tb >= tfull_max) break;                              // warp-uniform
 #pragma unroll
-    for (int j = 0; j < kShortG64; j++) {
+    for (int j = 0; j < G; j++) {
       const int t = tb + j;
       if (t >= 16) break;                                    // compile-time
       const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
