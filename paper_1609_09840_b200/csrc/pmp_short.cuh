@@ -194,7 +194,10 @@ constexpr int kTile = 32 * kShortWarps * kPasses;              // 384
 #ifndef PMP_SHORT_SLOTS
 #define PMP_SHORT_SLOTS 8
 #endif
-constexpr int kRing = PMP_SHORT_SLOTS, kOffAhead = PMP_SHORT_SLOTS / 2;  // tile slots (power of 2), offsets prefetch
+#ifndef PMP_SHORT_OFF_AHEAD
+#define PMP_SHORT_OFF_AHEAD (PMP_SHORT_SLOTS / 2)
+#endif
+constexpr int kRing = PMP_SHORT_SLOTS, kOffAhead = PMP_SHORT_OFF_AHEAD;  // tile slots (power of 2), offsets prefetch
 constexpr uint32_t kByteRing = PMP_SHORT_RING_KB * 1024;
 // Block-wide counting sort of each tile by word count before hashing
 // (PMP_SHORT_SORT=1): removes most of the zero-padding multiply-adds but costs
