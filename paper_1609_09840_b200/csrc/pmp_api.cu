@@ -671,11 +671,11 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     return PMP_EINVAL;
   const int sms = sm_count(k->device);
   Scratch sc(st), sc_off(st);
-  // work list (n u32) + counters [mid, big, then per schedule: next big, next mid batch]
+  // work list (n u32) + counters [mid, big, then per schedule: next big, next mid batch; k_short tile claims]
   if (sc.alloc((size_t)n * 4 + 32)) return PMP_ENOMEM;
   uint32_t *wcount = (uint32_t *)sc.p;
   uint32_t *wlist = wcount + 8;
-  if (cudaMemsetAsync(wcount, 0, 24, st) != cudaSuccess) return PMP_ECUDA;
+  if (cudaMemsetAsync(wcount, 0, 28, st) != cudaSuccess) return PMP_ECUDA;
   ParamKeys pk = param_keys(k);
   if (dual) {
     for (int i = 0; i < 32; i++) pk.a32[i] = (uint32_t)k2->a[i];

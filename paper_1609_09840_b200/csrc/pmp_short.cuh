@@ -209,10 +209,11 @@ constexpr uint32_t kByteRing = PMP_SHORT_RING_KB * 1024;
 constexpr uint32_t kSpanMaxTile = kByteRing / 2 < 32 * 1024 ? kByteRing / 2 : 32 * 1024;  // larger spans go direct
 constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
 constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
+constexpr uint32_t kModeEnd = 2;
 struct TileHdr {
   uint64_t alo;    // global address of staged byte 0
   uint32_t pos;    // ring position of staged byte 0
-  uint32_t mode;   // 0 staged, 1 direct
+  uint32_t mode;   // bits 0-1: 0 staged, 1 direct; bits 2-31: tile index; kModeEnd: no more tiles
 };
 constexpr size_t kShortSmem = 384 /* keys */ + kByteRing + kSlack + 16 + (size_t)kRing * kOffBytes +
                               (size_t)kRing * sizeof(TileHdr) +
@@ -251,9 +252,13 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   }
   __syncthreads();
   const uint32_t ntiles = (uint32_t)((n + kTile - 1) / kTile);
-  // tiles of this block: blockIdx.x + k * gridDim.x
-  const uint32_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  auto tile_base = [&](uint32_t k) { return ((uint64_t)blockIdx.x + (uint64_t)k * gridDim.x) * kTile; };
+  // Tiles are claimed dynamically (one global counter, wcount[6]) by the
+  // producer when it fetches their offsets, so blocks that run faster take more
+  // tiles: a static grid-stride split left 18% of the warp slots idle at the
+  // end (ncu achieved occupancy 27.8 of 34 warps).  Slot k of the ring holds
+  // the block's k-th claimed tile; a failed claim ends the block (kModeEnd).
+  uint32_t *const tile_ctr = wcount + 6;
+  __shared__ uint32_t tids[kRing];                     // claimed tile of each slot (producer)
   auto off_slot = [&](uint32_t k) { return offs + (size_t)(k & (kRing - 1)) * (kOffBytes / 8); };
 
   if (wib == kShortWarps) {
@@ -261,11 +266,20 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     auto wait_done = [&](uint32_t k) {  // tile k fully consumed
       mbar_wait(&bar_done[k & (kRing - 1)], (k / kRing) & 1);
     };
+    uint32_t k_end = 0xffffffffu;            // first slot whose claim failed (warp-uniform)
     auto issue_offs = [&](uint32_t k) {
       if (k >= kRing) wait_done(k - kRing);  // slot reuse
+      uint32_t t = 0;
+      if (lane == 0) t = atomicAdd(tile_ctr, 1u);
+      t = __shfl_sync(FULL, t, 0);
+      if (t >= ntiles) {
+        k_end = k;
+        return;
+      }
       if (lane == 0) {
         const int q = (int)(k & (kRing - 1));
-        const uint64_t base = tile_base(k);
+        tids[q] = t;
+        const uint64_t base = (uint64_t)t * kTile;
         const uint64_t cnt = min((uint64_t)kTile + 1, n + 1 - base);
         const uint32_t nb = (uint32_t)((cnt * 8 + 15) & ~15ULL);
         mbar_arrive_tx(&bar_off[q], nb);
@@ -276,12 +290,22 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     // tile k's bytes end at tend[k % kRing]; `oldest` is the first unreleased tile.
     uint32_t head = 0, tail = 0, oldest = 0;
     __shared__ uint32_t tend[kRing];
-    for (uint32_t k = 0; k < (uint32_t)kOffAhead && k < my_tiles; k++) issue_offs(k);
-    for (uint32_t k = 0; k < my_tiles; k++) {
+    for (uint32_t k = 0; k < (uint32_t)kOffAhead && k_end == 0xffffffffu; k++) issue_offs(k);
+    for (uint32_t k = 0;; k++) {
       const int q = (int)(k & (kRing - 1));
-      if (k + kOffAhead < my_tiles) issue_offs(k + kOffAhead);
+      if (k_end == 0xffffffffu) issue_offs(k + kOffAhead);
+      if (k == k_end) {                      // no more tiles: tell the consumers
+        __syncwarp();
+        if (lane == 0) {
+          hdr[q].mode = kModeEnd;
+          mbar_arrive_tx(&bar_full[q], 0);
+        }
+        break;
+      }
       mbar_wait(&bar_off[q], (k / kRing) & 1);
-      const uint64_t base = tile_base(k);
+      __syncwarp();
+      const uint32_t tid = tids[q];
+      const uint64_t base = (uint64_t)tid * kTile;
       const uint32_t nv = (uint32_t)min((uint64_t)kTile, n - base);  // strings in this tile
       const uint64_t *o = off_slot(k);
       // span of the tile and its place in the byte ring
@@ -317,7 +341,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         tend[q] = head;
         hdr[q].alo = (uint64_t)alo;
         hdr[q].pos = pos;
-        hdr[q].mode = mode;
+        hdr[q].mode = mode | (tid << 2);     // the consumers' tile index
         mbar_arrive_tx(&bar_full[q], nb);   // release: hdr and offsets visible to consumers
         if (nb) bulk_g2s(ring + pos, reinterpret_cast<const void *>(alo), nb, &bar_full[q]);
       }
@@ -330,19 +354,20 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   const uint32_t ring_s = smem_u32(ring);
   const uint32_t offs_s = smem_u32(offs) + 8u * (32u * wib + lane);
   const uint32_t hdr_s = smem_u32(hdr), full_s = smem_u32(bar_full), done_s = smem_u32(bar_done);
-  const uint64_t tstride = (uint64_t)gridDim.x * kTile;
   const uint32_t ct = 32u * wib + lane;                 // consumer thread = string slot in the tile
 #if PMP_SHORT_SORT
   const uint32_t offs0_s = smem_u32(offs), hist_s = smem_u32(s_hist), perm_s = smem_u32(s_perm);
 #endif
-  uint64_t ibase = (uint64_t)blockIdx.x * kTile;
-  for (uint32_t k = 0; k < my_tiles; k++, ibase += tstride) {
+  for (uint32_t k = 0;; k++) {
     const uint32_t q = k & (kRing - 1);
-    uint64_t i = ibase + ct;
     mbar_wait_s(full_s + 8 * q, (k / kRing) & 1);
     uint64_t ralo;
     uint32_t rpos, mode;
     lds_hdr(hdr_s + 16 * q, ralo, rpos, mode);
+    if (mode == kModeEnd) break;
+    const uint64_t ibase = (uint64_t)(mode >> 2) * kTile;
+    mode &= 3;
+    uint64_t i = ibase + ct;
     bool valid = i < n;
     uint64_t o0, o1;
     lds_u64x2(offs_s + q * kOffBytes, o0, o1);      // offsets[i], offsets[i+1] (slot-local)
