@@ -177,7 +177,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
 
 // k_short: warp-specialised TMA pipeline.  A block = 1 producer warp + kShortWarps
 // consumer warps, working on tiles of kTile = 32 * kShortWarps consecutive
-// strings (grid-strided).  Shared memory holds
+// strings (claimed dynamically, see below).  Shared memory holds
 //   - an offsets ring (kRing slots): the kTile+1 offsets of tile k, one TMA bulk
 //     copy issued kOffAhead tiles ahead;
 //   - a byte ring (kByteRing bytes): the 16-byte aligned contiguous byte span of
