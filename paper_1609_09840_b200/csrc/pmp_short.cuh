@@ -293,7 +293,6 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     for (uint32_t k = 0; k < (uint32_t)kOffAhead && k_end == 0xffffffffu; k++) issue_offs(k);
     for (uint32_t k = 0;; k++) {
       const int q = (int)(k & (kRing - 1));
-      if (k_end == 0xffffffffu) issue_offs(k + kOffAhead);
       if (k == k_end) {                      // no more tiles: tell the consumers
         __syncwarp();
         if (lane == 0) {
@@ -346,6 +345,9 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         if (nb) bulk_g2s(ring + pos, reinterpret_cast<const void *>(alo), nb, &bar_full[q]);
       }
       __syncwarp();
+      // claim + offsets of tile k + kOffAhead after tile k's bytes are on their
+      // way (the claim is a global atomic round trip)
+      if (k_end == 0xffffffffu) issue_offs(k + kOffAhead);
     }
     return;
   }
