@@ -199,13 +199,8 @@ constexpr int kTile = 32 * kShortWarps * kPasses;              // 384
 #endif
 constexpr int kRing = PMP_SHORT_SLOTS, kOffAhead = PMP_SHORT_OFF_AHEAD;  // tile slots (power of 2), offsets prefetch
 constexpr uint32_t kByteRing = PMP_SHORT_RING_KB * 1024;
-// Block-wide counting sort of each tile by word count before hashing
-// (PMP_SHORT_SORT=1): removes most of the zero-padding multiply-adds but costs
-// two named barriers per tile; measured 4-10% slower on configs[1]
-// (profiles/r01_summary.md), so it is off.
-#ifndef PMP_SHORT_SORT
-#define PMP_SHORT_SORT 0
-#endif
+// (Length sorting / partitioning of the tiles, to cut the zero-padding
+// multiply-adds, was measured five ways and never paid: profiles/r01f.)
 constexpr uint32_t kSpanMaxTile = kByteRing / 2 < 32 * 1024 ? kByteRing / 2 : 32 * 1024;  // larger spans go direct
 constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
 constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
@@ -217,7 +212,7 @@ struct TileHdr {
 };
 constexpr size_t kShortSmem = 384 /* keys */ + kByteRing + kSlack + 16 + (size_t)kRing * kOffBytes +
                               (size_t)kRing * sizeof(TileHdr) +
-                              (size_t)(3 * kRing) * 8 + (PMP_SHORT_SORT ? 256 /* sort histograms */ + 2 * kTile /* permutation */ : 0) + 128;
+                              (size_t)(3 * kRing) * 8 + 128;
 
 // DUAL: BITS = 64 and a second, 32-bit schedule in K.a32 / K.b32 whose digests go to os2
 template <int BITS, bool V2 = false, bool DUAL = false>
@@ -237,11 +232,6 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   uint64_t *bar_full = bar_done + kRing;                           // tile ready (consumers)
   if (threadIdx.x < 32) skeys[threadIdx.x] = K.a[threadIdx.x];
   if (DUAL && threadIdx.x < 32) skeys32[threadIdx.x] = K.a32[threadIdx.x];
-#if PMP_SHORT_SORT
-  uint32_t *s_hist = reinterpret_cast<uint32_t *>(bar_full + kRing);  // 2 x 32 class counters
-  uint16_t *s_perm = reinterpret_cast<uint16_t *>(s_hist + 64);      // kTile sorted slots
-  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
-#endif
   if (threadIdx.x == 0) {
     for (int q = 0; q < kRing; q++) {
       mbar_init(&bar_off[q], 1);
@@ -357,9 +347,6 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   const uint32_t offs_s = smem_u32(offs) + 8u * (32u * wib + lane);
   const uint32_t hdr_s = smem_u32(hdr), full_s = smem_u32(bar_full), done_s = smem_u32(bar_done);
   const uint32_t ct = 32u * wib + lane;                 // consumer thread = string slot in the tile
-#if PMP_SHORT_SORT
-  const uint32_t offs0_s = smem_u32(offs), hist_s = smem_u32(s_hist), perm_s = smem_u32(s_perm);
-#endif
   for (uint32_t k = 0;; k++) {
     const uint32_t q = k & (kRing - 1);
     mbar_wait_s(full_s + 8 * q, (k / kRing) & 1);
@@ -393,39 +380,6 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
       if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
       if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
     }
-#if PMP_SHORT_SORT
-    // ---- counting sort of the tile's strings by word count (block-wide, two
-    // named barriers): warp w then hashes sorted strings 32w..32w+31, whose
-    // word counts differ by at most one class, so the word loop below runs
-    // to (almost) every lane's own length instead of the longest string of
-    // 32 random ones.  Long / past-n strings sort last and are skipped.
-    {
-      const uint32_t cls = is_short ? min(B / (uint32_t)(BITS / 8), 30u) : 31u;
-      const uint32_t hb = hist_s + 128u * (k & 1);
-      const uint32_t rank = atoms_add(hb + 4 * cls, 1u);
-      named_bar_sync(1, kShortWarps * 32);
-      const uint32_t h = lds_u32(hb + 4 * lane);
-      uint32_t incl = h;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, incl, d);
-        if (lane >= d) incl += t;
-      }
-      const uint32_t start = __shfl_sync(FULL, incl - h, (int)cls);
-      sts_u16(perm_s + 2 * (start + rank), (uint16_t)ct);
-      named_bar_sync(1, kShortWarps * 32);
-      if (ct < 32) sts_u32(hb + 4 * ct, 0u);
-      const uint32_t j = lds_u16(perm_s + 2 * ct);
-      uint64_t p0, p1;
-      lds_u64x2(offs0_s + q * kOffBytes + 8 * j, p0, p1);
-      i = ibase + j;
-      valid = i < n;
-      o0 = p0;
-      const uint64_t Bj = valid ? p1 - p0 : 0;
-      is_short = Bj <= kShortMax;
-      B = (uint32_t)Bj;
-    }
-#endif
     // warp max of the number of full words (the marker word is handled apart)
     const int tfm = (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
     if (is_short) {
