@@ -534,3 +534,30 @@ def test_entry_points_edge_cases(torch_dev, oracle_lib):
     assert np.array_equal(got, oracle_batch(oracle_lib, 5, 64, big.cpu().numpy(), off))
     assert pmp.pmp_hash_batch(k64.handle, 0, d_off.data_ptr(), 3, d_off.data_ptr(), 0) == pmp.PMP_EINVAL
     assert pmp.pmp_hash_batch_multi([k64.handle], big.data_ptr(), d_off.data_ptr(), 3, [0], 0) == pmp.PMP_EINVAL
+
+
+@pytest.mark.parametrize("n", [511, 512, 513, 1024, 1025, 296 * 512 - 1, 296 * 512 + 1, 3 * 296 * 512 + 77])
+def test_short_tile_claims_at_tile_boundaries(torch_dev, oracle_lib, n):
+    """k_short claims its 512-string tiles dynamically (one global counter; a
+    failed claim ends the block; single-width kernels claim one call ahead):
+    string counts around tile multiples and beyond one tile per resident block
+    hash every string exactly once -- fused two-width pass and both single
+    widths, bit-exact against the oracle."""
+    import torch
+
+    rng = np.random.default_rng(n)
+    lens = rng.integers(0, 128, size=n).astype(np.uint64)
+    lens[rng.integers(0, n, size=max(1, n // 5000))] = 3000  # a few work-list strings
+    off = datagen.offsets_from_lengths(lens) + int(rng.integers(0, 16))
+    pay = datagen.payload_host(n, 0, int(off[-1]))
+    k64, k32 = pmp.Keys.generate(21, 64), pmp.Keys.generate(22, 32)
+    want64 = oracle_batch(oracle_lib, 21, 64, pay, off)
+    want32 = oracle_batch(oracle_lib, 22, 32, pay, off)
+    d_pay = torch.from_numpy(pay).to(torch_dev)
+    d_off = torch.from_numpy(off.view(np.int64)).to(torch_dev)
+    o64, o32 = pmp.hash_batch_multi([k64, k32], d_pay, d_off)
+    torch.cuda.synchronize()
+    assert np.array_equal(pmp.as_u64(o64), want64)
+    assert np.array_equal(pmp.as_u64(o32), want32)
+    assert np.array_equal(run_batch(torch_dev, k64, pay, off), want64)
+    assert np.array_equal(run_batch(torch_dev, k32, pay, off), want32)
