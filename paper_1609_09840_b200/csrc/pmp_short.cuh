@@ -205,6 +205,9 @@ constexpr uint32_t kSpanMaxTile = kByteRing / 2 < 32 * 1024 ? kByteRing / 2 : 32
 constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
 constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
 constexpr uint32_t kModeEnd = 2;
+#ifndef PMP_SHORT_DIAG
+#define PMP_SHORT_DIAG 0
+#endif
 struct TileHdr {
   uint64_t alo;    // global address of staged byte 0
   uint32_t pos;    // ring position of staged byte 0
@@ -262,7 +265,11 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     // producer's other work (every fired claim is read: a call follows until a
     // claim fails); separate widths 0.420 -> 0.407 ms.  The fused dual-width
     // kernel measured 0.7% slower that way and claims when it needs the tile.
+#ifdef PMP_CLAIM_AHEAD
+    constexpr bool kClaimAhead = PMP_CLAIM_AHEAD;
+#else
     constexpr bool kClaimAhead = !DUAL;
+#endif
     uint32_t claim = 0;
     if (kClaimAhead && lane == 0) claim = atomicAdd(tile_ctr, 1u);
     auto issue_offs = [&](uint32_t k) {
@@ -398,6 +405,11 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         const uint32_t sofs = rpos + (valid ? (uint32_t)((uintptr_t)(bytes + o0) - (uintptr_t)ralo) : 0u);
         const uint32_t pa = ring_s + (sofs & ~3u);
         auto fetch = [&](int kk) { return lds_u32(pa + 4 * kk); };
+#if PMP_SHORT_DIAG  // diagnostic build: the data pipeline alone (one shared load per string, no hashing)
+        lo = fetch(0) ^ B;
+        lo32 = (uint32_t)lo;
+        if (0)
+#endif
         if constexpr (DUAL) short_tree_dual<V2>(K, skeys, skeys32, B, 8 * (sofs & 3), tfm, fetch, lo, lo32);
         else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (sofs & 3), tfm, fetch);
       } else {
