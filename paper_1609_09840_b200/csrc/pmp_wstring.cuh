@@ -107,6 +107,9 @@ constexpr size_t kWSmem = kWBlockRegion + kWBlockWarps * kWSmemPerWarp;
 // POLY (reading Q19): C = T1 <= 128 gives Q = 1 virtual node, d = 128 - C,
 // and chunk c weighs W[c + d] = r^(C - c); every string (T1 = 1 included)
 // gets V = b_2 + sum.
+#ifndef PMP_M_DIAG
+#define PMP_M_DIAG 0
+#endif
 constexpr int kMPiece = 1024;                  // bytes per group per iteration
 constexpr int kMSlot = kMPiece + 32;           // + 16 B overlap + 16 B read slack
 #ifndef PMP_M_STAGES
@@ -301,6 +304,16 @@ __device__ PMP_MID_INLINE void mid_phase(const uint64_t *__restrict__ keys, cons
       constexpr bool kDupTail = POLY;
       uint4 U[4];
       auto mac_half = [&](uint4 (&U)[4]) {
+#if PMP_M_DIAG  // diagnostic build: the mid-phase pipeline alone (units folded by XOR, no multiply-adds)
+        if constexpr (BITS == 64) {
+#pragma unroll
+          for (int j = 0; j < 4; j++) A64.L ^= ((uint64_t)U[j].y << 32 | U[j].x) ^ ((uint64_t)U[j].w << 32 | U[j].z);
+        } else {
+          Acc3 A = {U[0].x ^ U[1].y ^ U[2].z ^ U[3].w, 0, 0};
+          part[hp < CPG ? hp : 0] = A;
+        }
+        return;
+#endif
         if (fix) {
           if (!active) {
 #pragma unroll
