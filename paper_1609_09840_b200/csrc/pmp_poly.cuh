@@ -54,14 +54,24 @@ PMP_DI typename Tr<BITS>::Acc poly_nodes(const uint64_t *__restrict__ keys, cons
   const uint64_t Qp = (C + d) / 128;
   Acc sum;
   acc_zero(sum);
-  for (uint64_t q = q_begin; q < q_end; q += q_step) {
+  if (q_begin >= q_end) return sum;
+  // The warp visits its nodes last to first, so the weight R^(Q'-1-q) grows by
+  // the constant factor R^q_step per node: one multiply per node instead of a
+  // ladder product of up to 17 (same value in every lane).
+  const uint64_t nt = (q_end - 1 - q_begin) / q_step + 1, q_last = q_begin + (nt - 1) * q_step;
+  Fe Rp = poly_pow_R<BITS>(keys, Qp - 1 - q_last);
+  const Fe Rstep = nt > 1 ? poly_pow_R<BITS>(keys, q_step) : Rp;
+  for (uint64_t t = nt; t-- > 0;) {
+    const uint64_t q = q_begin + t * q_step;
     const uint64_t first = q * 128 >= d ? q * 128 - d : 0;
     const uint64_t lo = max(first, cb), hi = min(q * 128 + 128 - d, ce);
-    if (lo >= hi) continue;
-    ChunkOut<BITS> co = warp_chunks<BITS, true, true>(s, lo, hi, lk, keys[0], keys + kPolyW, lane, d);
-    Fe nv = acc_reduce(co.acc2);
-    if (q + 1 < Qp) nv = fe_mul(nv, poly_pow_R<BITS>(keys, Qp - 1 - q));  // same value in every lane
-    acc_add_fe(sum, nv);
+    if (lo < hi) {
+      ChunkOut<BITS> co = warp_chunks<BITS, true, true>(s, lo, hi, lk, keys[0], keys + kPolyW, lane, d);
+      Fe nv = acc_reduce(co.acc2);
+      if (q + 1 < Qp) nv = fe_mul(nv, Rp);
+      acc_add_fe(sum, nv);
+    }
+    if (t) Rp = fe_mul(Rp, Rstep);
   }
   return sum;
 }

@@ -130,7 +130,8 @@ def test_fixed4k_full_size_sampled(dev, oracle_lib):
 def test_long16g_full(dev, oracle_lib):
     """configs[3]: one 16 GiB string, PM+64, seed 4 (reading Q16).  The digest of
     pmp_hash_long equals the oracle's literal Algorithm 1 over all 16 GiB, and
-    the G = 2, 4, 8 block-aligned splits (partial + combine) give the same."""
+    the G = 2, 4, 8 block-aligned splits (partial + combine) give the same; the
+    two-level variant's digest of the same string equals the oracle's."""
     import torch
 
     wl = datagen.WORKLOADS["long16g"]
@@ -154,11 +155,17 @@ def test_long16g_full(dev, oracle_lib):
             pos += c
         assert int(pmp.as_u64(st.final())[0]) == got, len(cuts)
         st.close()
+    # the two-level variant (8(f4)) over the same 16 GiB: 131,072 virtual nodes,
+    # more than the resident warps, so warps walk several nodes (weights
+    # R^(Q'-1-q) stepped by R^q_step)
+    got2 = int(pmp.as_u64(pmp.hash2_long(keys, buf, total))[0])
     del buf
     torch.cuda.empty_cache()
     host = host_payload_parallel(wl.seed, 0, total)
-    want = oracle_lib.hash_long(oracle_lib.keygen(wl.seed, 64), host, nthreads=NT)
+    okeys = oracle_lib.keygen(wl.seed, 64)
+    want = oracle_lib.hash_long(okeys, host, nthreads=NT)
     assert got == want
+    assert got2 == oracle_lib.hash2(okeys, host, nthreads=NT)
 
 
 def test_mixed_shard_sampled(dev, oracle_lib):
