@@ -285,6 +285,8 @@ def main():
                     help="long16g only (SURVEY 8(f1)): feed the string through pmp_stream_update in pieces of this many MiB")
     ap.add_argument("--buckets", type=int, default=0,
                     help="hash-table consumer (SURVEY 8(f3)): write digest mod M + histogram instead of digests")
+    ap.add_argument("--partition", action="store_true",
+                    help="with --buckets: also group the string indices by bucket (pmp_bucket_partition)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--variant", default="tree", choices=["tree", "two-level"],
                     help="two-level: the multilinear + polynomial variant (8(f4), pmp_hash2_*)")
@@ -390,6 +392,10 @@ def main():
         payload_bytes = total_bytes * len(wl.bits)
 
         counts = torch.zeros(max(args.buckets, 1), dtype=torch.int32, device=dev)
+        assert not args.partition or args.buckets, "--partition needs --buckets M"
+        if args.partition:
+            p_starts = torch.empty(args.buckets + 1, dtype=torch.int64, device=dev)
+            p_perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
 
         fused = len(wl.bits) == 2 and not args.buckets and not args.separate_widths
         fused_dual = fused
@@ -406,6 +412,10 @@ def main():
                     pmp._check(pmp.pmp_hash_batch_buckets(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
                                                           args.buckets, outs[b].data_ptr(), counts.data_ptr(), sp),
                                "pmp_hash_batch_buckets")
+                    if args.partition:
+                        pmp._check(pmp.pmp_bucket_partition(outs[b].data_ptr(), n, args.buckets, 0,
+                                                            p_starts.data_ptr(), p_perm.data_ptr(), sp),
+                                   "pmp_bucket_partition")
                 else:
                     fn = pmp.pmp_hash2_batch if v2 else pmp.pmp_hash_batch
                     pmp._check(fn(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
@@ -440,7 +450,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
     k_ms, k_cnt = pmp.pmp_prof_read(dominant)
     kernel_ms = {name: pmp.pmp_prof_read(name) for name in ("k_short", "k_wstring", "k_histogram", "k_node", "k_level", "k_combine",
-                                                             "k_stream", "k_poly")}
+                                                             "k_stream", "k_poly", "k_part")}
     t = torch.tensor([ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -474,7 +484,8 @@ def main():
             "scaling": "strong" if wl.long else "weak", "vs_baseline": None,
             "dtype": "u64+u32" if len(wl.bits) > 1 else f"u{wl.bits[0]}",
             "data": "synthetic (seeded xoshiro256** bytes, generated on device)",
-            "config": dict(workload_config(wl, world, args.variant), **({"output": f"buckets mod {args.buckets} + histogram"}
+            "config": dict(workload_config(wl, world, args.variant), **({"output": f"buckets mod {args.buckets} + histogram"
+                                                                     + (" + partition" if args.partition else "")}
                                                           if args.buckets else {}),
                            **({"api": f"pmp_stream_update in {args.stream_mib} MiB pieces"} if args.stream_mib else {})),
             "bytes_per_gpu_cycle": (value / world * 1e9) / (clocks["sm_mhz"] * 1e6) if clocks.get("sm_mhz") else None,

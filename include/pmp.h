@@ -121,6 +121,24 @@ int pmp_hash_batch_buckets(const pmp_keys *keys, const uint8_t *bytes, const uin
                            uint64_t n, uint32_t M, uint32_t *buckets, uint32_t *counts,
                            struct CUstream_st *stream);
 
+/* Bucket partition, the step after the histogram in a GPU hash join /
+ * group-by (the paper's motivating use):
+ * the string indices 0..n-1 grouped by bucket id.
+ *   buckets (device) n uint32, each < M (e.g. from pmp_hash_batch_buckets; an
+ *           id >= M is a precondition violation, not checked);
+ *   hist    (device) M uint32, the bucket sizes of exactly these n ids (e.g. the
+ *           counts of one pmp_hash_batch_buckets call into zeroed counters), or
+ *           NULL: the library counts them (one more pass over the ids);
+ *   starts  (device, out) M+1 uint64: bucket b occupies perm[starts[b],
+ *           starts[b+1]) (exclusive prefix sums of the bucket sizes); starts[M] = n;
+ *   perm    (device, out) n uint32: the indices, bucket by bucket; the order
+ *           inside a bucket is unspecified (it depends on scheduling).
+ * 1 <= M <= 2^24 and n < 2^32, else PMP_EINVAL (also for NULL with n > 0);
+ * n = 0 writes starts (all zero).  Runs on the current device, stream-ordered;
+ * scratch (M counters) is stream-allocated.  PMP_ENODEV without a device. */
+int pmp_bucket_partition(const uint32_t *buckets, uint64_t n, uint32_t M, const uint32_t *hist,
+                         uint64_t *starts, uint32_t *perm, struct CUstream_st *stream);
+
 #define PMP_HOST_MAX_KEYS 4
 /* Several key schedules over one device batch (1 <= nkeys <= PMP_HOST_MAX_KEYS;
  * outs[k]: device, n digests for keys[k]).  Equal to nkeys pmp_hash_batch

@@ -51,6 +51,7 @@ def lib() -> ctypes.CDLL:
             "pmp_keys_free": ([_vp], None),
             "pmp_hash_batch": ([_vp, _vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_batch_buckets": ([_vp, _vp, _vp, _u64, ctypes.c_uint32, _vp, _vp, _vp], _int),
+            "pmp_bucket_partition": ([_vp, _u64, ctypes.c_uint32, _vp, _vp, _vp, _vp], _int),
             "pmp_hash_batch_host": ([_vp, _int, _vp, _vp, _u64, _vp, _u64, _vp], _int),
             "pmp_hash_batch_multi": ([_vp, _int, _vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash2_batch_multi": ([_vp, _int, _vp, _vp, _u64, _vp, _vp], _int),
@@ -153,6 +154,11 @@ def pmp_hash_batch_host(keys: list, bytes_ptr: int, offsets_ptr: int, n: int, ou
 def pmp_hash_batch_buckets(keys: int, bytes_ptr: int, offsets_ptr: int, n: int, M: int, buckets_ptr: int,
                            counts_ptr: int, stream: int) -> int:
     return lib().pmp_hash_batch_buckets(keys, bytes_ptr, offsets_ptr, n, M, buckets_ptr, counts_ptr, stream)
+
+
+def pmp_bucket_partition(buckets_ptr: int, n: int, M: int, hist_ptr: int, starts_ptr: int, perm_ptr: int,
+                         stream: int = 0) -> int:
+    return lib().pmp_bucket_partition(buckets_ptr, n, M, hist_ptr, starts_ptr, perm_ptr, stream)
 
 
 def pmp_hash_long(keys: int, bytes_ptr: int, length: int, out_ptr: int, stream: int) -> int:
@@ -365,6 +371,21 @@ def hash_batch_buckets(keys: Keys, payload, offsets, M: int, counts=None, out=No
                                   out.data_ptr(), counts.data_ptr() if counts is not None else 0,
                                   _stream_ptr(stream)), "pmp_hash_batch_buckets")
     return out
+
+
+def bucket_partition(buckets, M: int, hist=None, stream=None):
+    """String indices grouped by bucket id (pmp_bucket_partition): returns
+    (starts, perm) -- int64 tensor of M+1 bucket starts and int32 tensor (holding
+    uint32) of the n indices, bucket by bucket (order inside a bucket
+    unspecified).  ``hist``: optional int32 tensor of the M bucket sizes."""
+    import torch
+
+    n = buckets.numel()
+    starts = torch.empty(M + 1, dtype=torch.int64, device=buckets.device)
+    perm = torch.empty(max(n, 1), dtype=torch.int32, device=buckets.device)
+    _check(pmp_bucket_partition(buckets.data_ptr(), n, M, hist.data_ptr() if hist is not None else 0,
+                                starts.data_ptr(), perm.data_ptr(), _stream_ptr(stream)), "pmp_bucket_partition")
+    return starts, perm[:n]
 
 
 def hash_long(keys: Keys, data, length: int | None = None, out=None, stream=None):

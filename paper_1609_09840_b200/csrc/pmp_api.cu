@@ -773,6 +773,37 @@ int pmp_hash_batch_buckets(const pmp_keys *k, const uint8_t *bytes, const uint64
                 [&] { k_histogram<<<(unsigned)grid, 512, smem, st>>>(buckets, n, M, counts); });
 }
 
+int pmp_bucket_partition(const uint32_t *buckets, uint64_t n, uint32_t M, const uint32_t *hist, uint64_t *starts,
+                         uint32_t *perm, cudaStream_t st) {
+  if (M == 0 || M > (1u << 24) || !starts || n >= (1ULL << 32) || (n && (!buckets || !perm))) return PMP_EINVAL;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return PMP_ENODEV;
+  const int sms = sm_count(dev);
+  Scratch sc(st);
+  if (sc.alloc((size_t)M * 4)) return PMP_ENOMEM;
+  uint32_t *counts = (uint32_t *)sc.p;
+  const size_t smem = M <= kHistSmemMax ? (size_t)M * 4 : 0;
+  if (hist) {                                            // the caller's histogram of these buckets
+    if (cudaMemcpyAsync(counts, hist, (size_t)M * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return PMP_ECUDA;
+  } else if (cudaMemsetAsync(counts, 0, (size_t)M * 4, st) != cudaSuccess) {
+    return PMP_ECUDA;
+  }
+  if (n && !hist) {
+    uint64_t grid = (n + 511) / 512;
+    if (grid > (uint64_t)sms * 4) grid = (uint64_t)sms * 4;
+    if (int rc = launch("k_histogram", st,
+                        [&] { k_histogram<<<(unsigned)grid, 512, smem, st>>>(buckets, n, M, counts); }))
+      return rc;
+  }
+  if (int rc = launch("k_part_scan", st, [&] { k_part_scan<<<1, 1024, 0, st>>>(counts, M, n, starts); })) return rc;
+  if (n == 0) return 0;
+  uint64_t grid = M <= kHistSmemMax ? (n + kPartChunk - 1) / kPartChunk : (n + kPartThreads - 1) / kPartThreads;
+  if (grid > (uint64_t)sms * 4) grid = (uint64_t)sms * 4;
+  return launch("k_part_scatter", st, [&] {
+    k_part_scatter<<<(unsigned)grid, kPartThreads, smem, st>>>(buckets, n, M, counts, perm);
+  });
+}
+
 static int batch_multi_impl(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
                             uint64_t n, void *const *outs, cudaStream_t st, bool v2) {
   if (!keys || !outs || nkeys < 1 || nkeys > PMP_HOST_MAX_KEYS) return PMP_EINVAL;

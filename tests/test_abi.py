@@ -130,6 +130,18 @@ def test_bucket_call_rejects_zero_modulus(L):
     assert pmp.pmp_hash_batch_buckets(k.handle, 8, 8, 1, 0, 8, 0, 0) == pmp.PMP_EINVAL
 
 
+def test_bucket_partition_argument_checks(L):
+    """pmp_bucket_partition: M == 0, M > 2^24, NULL starts, NULL buckets/perm
+    with n > 0 and n >= 2^32 are PMP_EINVAL before any device work."""
+    E = pmp.PMP_EINVAL
+    assert pmp.pmp_bucket_partition(8, 10, 0, 0, 8, 8) == E
+    assert pmp.pmp_bucket_partition(8, 10, (1 << 24) + 1, 0, 8, 8) == E
+    assert pmp.pmp_bucket_partition(8, 10, 16, 0, 0, 8) == E
+    assert pmp.pmp_bucket_partition(0, 10, 16, 0, 8, 8) == E
+    assert pmp.pmp_bucket_partition(8, 10, 16, 0, 8, 0) == E
+    assert pmp.pmp_bucket_partition(8, 1 << 32, 16, 0, 8, 8) == E
+
+
 @pytest.mark.parametrize("bits,size", [(64, 8264), (32, 4136)])
 def test_keyfile_roundtrip_and_layout(L, bits, size):
     """KeyFile: exact size, header bytes, and the

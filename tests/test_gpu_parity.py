@@ -323,6 +323,42 @@ def test_buckets_and_histogram(torch_dev, oracle_lib, bits, M):
         assert np.array_equal(counts.cpu().numpy().astype(np.int64), np.bincount(want.astype(np.int64), minlength=M))
 
 
+@pytest.mark.parametrize("M,n", [(1, 3000), (7, 5000), (1024, 5000), (1024, 1 << 20), (12288, 200000),
+                                 (50000, 200000), (1 << 24, 70000)])
+def test_bucket_partition(torch_dev, oracle_lib, M, n):
+    """pmp_bucket_partition after pmp_hash_batch_buckets: starts
+    == exclusive prefix sums of the oracle buckets' bincount; perm is a
+    permutation of 0..n-1 whose oracle buckets are grouped in bucket order and
+    match starts (the order inside a bucket is free).  Covers the shared-memory
+    ranked path (M <= 12288) and the global-atomic path."""
+    import torch
+
+    rng = np.random.default_rng(M + n)
+    lens = rng.integers(0, 100, size=n).astype(np.uint64)
+    off = datagen.offsets_from_lengths(lens)
+    pay = datagen.payload_host(41, 0, int(off[-1]))
+    keys = pmp.Keys.generate(41, 64)
+    d_pay = torch.from_numpy(pay).to(torch_dev)
+    d_off = torch.from_numpy(off.view(np.int64)).to(torch_dev)
+    hist = torch.zeros(M, dtype=torch.int32, device=torch_dev) if M <= 65536 else None
+    b = pmp.hash_batch_buckets(keys, d_pay, d_off, M, counts=hist)
+    starts, perm = pmp.bucket_partition(b, M)
+    if hist is not None:                                   # the caller's histogram instead of a recount
+        starts2, perm2 = pmp.bucket_partition(b, M, hist=hist)
+        assert torch.equal(starts2, starts)
+        p2 = perm2.cpu().numpy().view(np.uint32).astype(np.int64)
+        assert np.array_equal(np.sort(p2), np.arange(n))
+    torch.cuda.synchronize()
+    ob = (oracle_batch(oracle_lib, 41, 64, pay, off).astype(np.uint64) % np.uint64(M)).astype(np.int64)
+    want_starts = np.concatenate([[0], np.cumsum(np.bincount(ob, minlength=M))])
+    assert np.array_equal(starts.cpu().numpy(), want_starts)
+    p = perm.cpu().numpy().view(np.uint32).astype(np.int64)
+    assert np.array_equal(np.sort(p), np.arange(n))
+    grouped = ob[p]
+    assert np.all(np.diff(grouped) >= 0)
+    assert np.array_equal(np.searchsorted(grouped, np.arange(M + 1), side="left"), want_starts)
+
+
 # ------------------------------------------------------------ quality suite (SURVEY 8(f2))
 @pytest.mark.parametrize("bits,length", [(64, 8), (64, 16), (32, 4), (32, 12)])
 def test_avalanche_bias_small(torch_dev, bits, length):
