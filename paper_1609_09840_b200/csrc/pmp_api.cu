@@ -799,8 +799,14 @@ int pmp_bucket_partition(const uint32_t *buckets, uint64_t n, uint32_t M, const 
   if (n == 0) return 0;
   uint64_t grid = M <= kHistSmemMax ? (n + kPartChunk - 1) / kPartChunk : (n + kPartThreads - 1) / kPartThreads;
   if (grid > (uint64_t)sms * 4) grid = (uint64_t)sms * 4;
+  const size_t psmem =
+      PMP_PART_STAGE && M >= kPartStageMin && M <= kPartStageMax ? (size_t)M * 8 + (size_t)kPartChunk * 6 : smem;
+  static std::once_flag part_attr;                       // 48 KB of counters + the static scan scratch
+  std::call_once(part_attr, [] {
+    cudaFuncSetAttribute(k_part_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  });
   return launch("k_part_scatter", st, [&] {
-    k_part_scatter<<<(unsigned)grid, kPartThreads, smem, st>>>(buckets, n, M, counts, perm);
+    k_part_scatter<<<(unsigned)grid, kPartThreads, psmem, st>>>(buckets, n, M, counts, perm);
   });
 }
 

@@ -109,6 +109,12 @@ namespace pmp {
 #endif
 constexpr int kPartThreads = 512, kPartPer = PMP_PART_PER;
 constexpr uint32_t kPartChunk = (uint32_t)kPartThreads * kPartPer;
+#ifndef PMP_PART_STAGE
+#define PMP_PART_STAGE 1
+#endif
+// buckets for the staged scatter (shared: 8 M + 6 chunk bytes); with fewer
+// buckets the direct writes already form long runs (measured faster, s43)
+constexpr uint32_t kPartStageMin = 128, kPartStageMax = 2048;
 
 __global__ void __launch_bounds__(1024)
 k_part_scan(uint32_t *__restrict__ counts, uint32_t M, uint64_t n, uint64_t *__restrict__ starts) {
@@ -155,6 +161,75 @@ k_part_scatter(const uint32_t *__restrict__ buckets, uint64_t n, uint32_t M, uin
       perm[atomicAdd(&cursor[__ldcs(buckets + i)], 1u)] = (uint32_t)i;
     return;
   }
+#if PMP_PART_STAGE
+  if (M >= kPartStageMin && M <= kPartStageMax) {
+    // staged: the chunk's indices are first placed in shared memory in bucket
+    // order (local prefix sums of the chunk's bucket sizes), then written out
+    // slot by slot, so consecutive threads write consecutive positions of a
+    // bucket's range instead of one scattered word each
+    uint32_t *g = h + M;                                  // global base per bucket (this chunk)
+    uint32_t *stage = g + M;                              // kPartChunk indices in bucket order
+    uint16_t *stage_b = reinterpret_cast<uint16_t *>(stage + kPartChunk);
+    __shared__ uint32_t s_wsum[kPartThreads / 32];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr uint32_t kPer = (kPartStageMax + kPartThreads - 1) / kPartThreads;
+    for (uint64_t c0 = (uint64_t)blockIdx.x * kPartChunk; c0 < n; c0 += (uint64_t)gridDim.x * kPartChunk) {
+      for (uint32_t b = threadIdx.x; b < M; b += blockDim.x) h[b] = 0;
+      __syncthreads();
+      uint32_t bk[kPartPer], rk[kPartPer];
+#pragma unroll
+      for (int j = 0; j < kPartPer; j++) {
+        const uint64_t i = c0 + (uint64_t)j * blockDim.x + threadIdx.x;
+        bk[j] = i < n ? __ldcs(buckets + i) : 0u;
+        rk[j] = i < n ? atomicAdd(&h[bk[j]], 1u) : 0u;
+      }
+      __syncthreads();
+      for (uint32_t b = threadIdx.x; b < M; b += blockDim.x)  // global ranges, in bucket order
+        g[b] = h[b] ? atomicAdd(&cursor[b], h[b]) : 0u;
+      // exclusive scan of h (thread t owns buckets [t kPer, (t+1) kPer)) -> local starts
+      const uint32_t b0 = threadIdx.x * kPer;
+      uint32_t loc = 0;
+#pragma unroll
+      for (uint32_t e = 0; e < kPer; e++) loc += b0 + e < M ? h[b0 + e] : 0u;
+      uint32_t incl = loc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, incl, d);
+        if ((int)lane >= d) incl += y;
+      }
+      if (lane == 31) s_wsum[wid] = incl;
+      __syncthreads();
+      uint32_t woff = 0;
+      for (uint32_t w = 0; w < wid; w++) woff += s_wsum[w];
+      uint32_t run = woff + incl - loc;
+#pragma unroll
+      for (uint32_t e = 0; e < kPer; e++)
+        if (b0 + e < M) {
+          const uint32_t c = h[b0 + e];
+          h[b0 + e] = run;                                // local start of the bucket
+          run += c;
+        }
+      __syncthreads();
+      const uint32_t nv = (uint32_t)min((uint64_t)kPartChunk, n - c0);
+#pragma unroll
+      for (int j = 0; j < kPartPer; j++) {
+        const uint64_t i = c0 + (uint64_t)j * blockDim.x + threadIdx.x;
+        if (i < n) {
+          const uint32_t sl = h[bk[j]] + rk[j];
+          stage[sl] = (uint32_t)i;
+          stage_b[sl] = (uint16_t)bk[j];
+        }
+      }
+      __syncthreads();
+      for (uint32_t sl = threadIdx.x; sl < nv; sl += blockDim.x) {
+        const uint32_t b = stage_b[sl];
+        perm[g[b] + (sl - h[b])] = stage[sl];
+      }
+      __syncthreads();
+    }
+    return;
+  }
+#endif
   for (uint64_t c0 = (uint64_t)blockIdx.x * kPartChunk; c0 < n; c0 += (uint64_t)gridDim.x * kPartChunk) {
     for (uint32_t b = threadIdx.x; b < M; b += blockDim.x) h[b] = 0;
     __syncthreads();
