@@ -53,8 +53,34 @@ def lib():
         h.pmpd_fill_device.restype = ctypes.c_int
         h.pmpd_fill_device_at.argtypes = [u64, vp, u64, u64, vp]
         h.pmpd_fill_device_at.restype = ctypes.c_int
+        h.pmpd_splitmix64_stream.argtypes = [u64, u64, vp]
+        h.pmpd_splitmix64_stream.restype = None
+        h.pmpd_xoshiro256ss_stream.argtypes = [vp, u64, vp]
+        h.pmpd_xoshiro256ss_stream.restype = None
+        h.pmpd_stream.argtypes = [u64, u64, u64, vp]
+        h.pmpd_stream.restype = None
         _lib = h
     return _lib
+
+
+def splitmix64_stream(state: int, n: int) -> list:
+    out = np.zeros(n, dtype=np.uint64)
+    lib().pmpd_splitmix64_stream(state & (2**64 - 1), n, out.ctypes.data)
+    return [int(x) for x in out]
+
+
+def xoshiro256ss_stream(state, n: int) -> list:
+    st = np.ascontiguousarray([int(x) & (2**64 - 1) for x in state], dtype=np.uint64)
+    out = np.zeros(n, dtype=np.uint64)
+    lib().pmpd_xoshiro256ss_stream(st.ctypes.data, n, out.ctypes.data)
+    return [int(x) for x in out]
+
+
+def stream(seed: int, sid: int, n: int) -> list:
+    """n outputs of stream(seed, id) (pmp_datagen.h contract)."""
+    out = np.zeros(n, dtype=np.uint64)
+    lib().pmpd_stream(seed & (2**64 - 1), sid & (2**64 - 1), n, out.ctypes.data)
+    return [int(x) for x in out]
 
 
 def lengths(kind: int, seed: int, n: int, lo: int, hi: int) -> np.ndarray:

@@ -78,6 +78,22 @@ extern "C" void pmpd_lengths(int kind, uint64_t seed, uint64_t n, uint64_t lo, u
   }
 }
 
+// Raw generator streams, exported so the tests can pin them to published
+// reference outputs (tests/golden/prng.txt).
+extern "C" void pmpd_splitmix64_stream(uint64_t state, uint64_t n, uint64_t *out) {
+  for (uint64_t i = 0; i < n; i++) out[i] = sm64(&state);
+}
+extern "C" void pmpd_xoshiro256ss_stream(const uint64_t *s, uint64_t n, uint64_t *out) {
+  Xo g;
+  g.s0 = s[0]; g.s1 = s[1]; g.s2 = s[2]; g.s3 = s[3];
+  for (uint64_t i = 0; i < n; i++) out[i] = g.next();
+}
+extern "C" void pmpd_stream(uint64_t seed, uint64_t id, uint64_t n, uint64_t *out) {
+  Xo g;
+  g.seed(seed, id);
+  for (uint64_t i = 0; i < n; i++) out[i] = g.next();
+}
+
 extern "C" uint64_t pmpd_offsets(const uint64_t *lengths, uint64_t n, uint64_t *offsets) {
   uint64_t acc = 0;
   offsets[0] = 0;

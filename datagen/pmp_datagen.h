@@ -35,6 +35,13 @@ enum pmpd_len_kind {
 void pmpd_lengths(int kind, uint64_t seed, uint64_t n, uint64_t lo, uint64_t hi,
                   uint64_t *lengths);
 
+/* The generators behind the contract (for pinning to published outputs):
+ * n splitmix64 outputs from `state`; n xoshiro256** outputs from s[4];
+ * n outputs of stream(seed, id). */
+void pmpd_splitmix64_stream(uint64_t state, uint64_t n, uint64_t *out);
+void pmpd_xoshiro256ss_stream(const uint64_t *s, uint64_t n, uint64_t *out);
+void pmpd_stream(uint64_t seed, uint64_t id, uint64_t n, uint64_t *out);
+
 /* CSR offsets: offsets[0] = 0, offsets[i+1] = offsets[i] + lengths[i].
  * Returns offsets[n]. */
 uint64_t pmpd_offsets(const uint64_t *lengths, uint64_t n, uint64_t *offsets);

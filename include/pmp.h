@@ -169,6 +169,20 @@ int pmp_hash_batch_multi(const pmp_keys *const *keys, int nkeys, const uint8_t *
 int pmp_hash_batch_host(const pmp_keys *const *keys, int nkeys, const uint8_t *bytes, const uint64_t *offsets,
                         uint64_t n, void *const *outs, uint64_t piece_bytes, struct CUstream_st *stream);
 
+/* Host-resident long string (the e2e path of configs[3]): the same digest as
+ * pmp_hash_long for `len` bytes at `bytes` in HOST memory.  The string is cut
+ * into pieces of piece_bytes (0: 256 MiB; rounded down to whole level-1
+ * blocks) that are copied host->device on internal streams into three device
+ * slots and fed to a device-resident incremental state (the pmp_stream_*
+ * machinery) on `stream`, so the copy of one piece overlaps the
+ * hashing of the previous one.  The digest (uint64 / uint32 by the keys'
+ * width) is written to `out_host` (HOST memory).  Stream-ordered: starts after
+ * prior work on `stream`; `out_host` holds the digest once `stream` has
+ * reached this point; `bytes` must stay valid until then.  `bytes` should be
+ * page-locked for the copies to run asynchronously.  Errors as pmp_hash_long. */
+int pmp_hash_long_host(const pmp_keys *keys, const uint8_t *bytes, uint64_t len, void *out_host,
+                       uint64_t piece_bytes, struct CUstream_st *stream);
+
 /* Hash one string of `len` bytes at `bytes` (device, any alignment); writes
  * one digest (uint64 / uint32) to `out` (device).  Block-parallel over the
  * level-2 nodes of the tree (128 level-1 blocks each), then one launch per
@@ -181,11 +195,15 @@ int pmp_hash_long(const pmp_keys *keys, const uint8_t *bytes, uint64_t len, void
  * The caller holds bytes [global_offset, global_offset + local_len) of a string
  * of total_len bytes at `local` (device).  global_offset must be a multiple of
  * the level-1 block size (1024 bytes for PM+64, 512 for PM+32) and so must
- * local_len unless global_offset + local_len == total_len (the caller owning the
- * tail, which also owns the marker word).  Writes to `partial` (device, 2
+ * local_len unless global_offset + local_len == total_len.  The tail block (the
+ * one holding the marker word) belongs to the one range that holds the
+ * last byte total_len - 1; an empty range never owns it, so any number of empty
+ * ranges may appear anywhere in the split.  Writes to `partial` (device, 2
  * uint64: lo, hi) the field element P = sum over the caller's blocks c of
  * K_c * v_1(c) mod p, where K_c is the product of the level keys on c's path
- * to the root.  Ranges of all callers must tile [0, total_len). */
+ * to the root (an empty range writes 0).  Ranges of all callers must tile
+ * [0, total_len).  For the empty message (total_len == 0) every partial is 0
+ * and the combine supplies the value sigma_0 = 1 (reading Q2). */
 int pmp_hash_long_partial(const pmp_keys *keys, const uint8_t *local, uint64_t local_len,
                           uint64_t global_offset, uint64_t total_len, uint64_t *partial,
                           struct CUstream_st *stream);
@@ -230,7 +248,10 @@ void pmp_stream_free(pmp_stream *s);
  *   pmp_hash2_long         ~ pmp_hash_long
  *   pmp_hash2_long_partial ~ pmp_hash_long_partial: the caller's chunks
  *       contribute sum v_c r^(C-c) (a field element, 2 words) -- no key-only
- *       constant is needed, the sum is linear in the v_c;
+ *       constant is needed, the sum is linear in the v_c.  The tail chunk
+ *       belongs to the range holding byte total_len - 1 (never to an empty
+ *       range); the empty message (total_len == 0, one marker-only chunk)
+ *       must be hashed as a single range;
  *   pmp_hash2_long_combine: digest of b_2 + sum_g P_g (G partials, device). */
 int pmp_hash2_batch(const pmp_keys *keys, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
                     void *out, struct CUstream_st *stream);
@@ -272,6 +293,15 @@ int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_
  * and returns the summed milliseconds and launch count of kernels whose name
  * starts with `prefix` ("k_short", "k_wstring", "k_node", ...). */
 uint64_t pmp_launch_count(void);
+
+/* Batch routing (tuning / test hook).  A batch call with n <= this threshold
+ * takes the latency path (k_small: one launch, no scratch, one thread per
+ * short string, one warp per longer string); larger batches take the
+ * throughput path (k_short's TMA pipeline + k_wstring).  Both give identical
+ * digests.  Default 4096; 0 sends every batch to the throughput path.  Sets
+ * the process-wide value and returns the previous one.  The two-level
+ * variant always takes the throughput path. */
+uint64_t pmp_set_small_batch_max(uint64_t n);
 void pmp_prof_enable(int on);
 void pmp_prof_reset(void);
 int pmp_prof_read(const char *prefix, double *ms, uint64_t *count);

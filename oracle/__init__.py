@@ -78,6 +78,10 @@ def lib():
         h.pmpo_hash2.restype = _u64
         h.pmpo_hash2_batch.argtypes = [ctypes.c_int, _p, _p, _p, _p, _u64, _p, ctypes.c_int]
         h.pmpo_hash2_batch.restype = None
+        h.pmpo_splitmix64_stream.argtypes = [_u64, _u64, _p]
+        h.pmpo_splitmix64_stream.restype = None
+        h.pmpo_xoshiro256ss_stream.argtypes = [_p, _u64, _p]
+        h.pmpo_xoshiro256ss_stream.restype = None
         h.pmpo_mulmod.argtypes = [_u64, _u64, _u64, _u64, _u64, _u64, _p]
         h.pmpo_mulmod.restype = None
         _lib = h
@@ -130,6 +134,21 @@ def keygen(seed: int, bits: int) -> Keys:
     if rc != 0:
         raise ValueError(bits)
     return Keys(bits, b, a)
+
+
+def splitmix64_stream(state: int, n: int) -> list:
+    """n successive splitmix64 outputs from ``state`` (the keygen contract's seeding)."""
+    out = np.zeros(n, dtype=np.uint64)
+    lib().pmpo_splitmix64_stream(state & (2**64 - 1), n, _ptr(out))
+    return [int(x) for x in out]
+
+
+def xoshiro256ss_stream(state, n: int) -> list:
+    """n successive xoshiro256** outputs from the 4-word state ``state``."""
+    st = np.ascontiguousarray([int(x) & (2**64 - 1) for x in state], dtype=np.uint64)
+    out = np.zeros(n, dtype=np.uint64)
+    lib().pmpo_xoshiro256ss_stream(_ptr(st), n, _ptr(out))
+    return [int(x) for x in out]
 
 
 def mix(bits: int, z: int) -> int:

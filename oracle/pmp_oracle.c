@@ -70,6 +70,16 @@ static uint64_t xoshiro_next(uint64_t s[4]) {
   return result;
 }
 
+/* The raw generator streams keygen draws from, exported so that tests can pin
+ * them to the published reference outputs (tests/golden/prng.txt). */
+void pmpo_splitmix64_stream(uint64_t state, uint64_t n, uint64_t *out) {
+  for (uint64_t i = 0; i < n; i++) out[i] = splitmix64_next(&state);
+}
+void pmpo_xoshiro256ss_stream(const uint64_t s_in[4], uint64_t n, uint64_t *out) {
+  uint64_t s[4] = {s_in[0], s_in[1], s_in[2], s_in[3]};
+  for (uint64_t i = 0; i < n; i++) out[i] = xoshiro_next(s);
+}
+
 int pmpo_keygen(uint64_t seed, int bits, uint64_t *b, uint64_t *a) {
   uint64_t a_max;
   if (pmpo_params(bits, NULL, NULL, NULL, NULL, &a_max) != 0) return -1;
@@ -254,24 +264,37 @@ static int tree_value_u128(int bits, const uint64_t *b, const uint64_t *a,
     return 0;
   }
   uint64_t n1 = (T + PMPO_M - 1) / PMPO_M; /* level 1: zero-pad, map f_1 */
+  l1_job one;
+  memset(&one, 0, sizeof(one));
+  one.bits = bits; one.p = p; one.b = b; one.a = a;
+  one.bytes = bytes; one.len = len; one.T = T;
+  one.c_begin = 0; one.c_end = n1;
+  if (n1 == 1) { /* a single level-1 block: its value is the tree value (no heap) */
+    u128 y0 = 0;
+    one.y = &y0;
+    l1_worker(&one);
+    *V = y0;
+    return 1;
+  }
   u128 *y = (u128 *)malloc(sizeof(u128) * (size_t)n1);
+  one.y = y;
   if (nthreads < 1) nthreads = 1;
   if ((uint64_t)nthreads > n1) nthreads = (int)n1;
-  l1_job *jobs = (l1_job *)calloc((size_t)nthreads, sizeof(l1_job));
-  pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
-  for (int i = 0; i < nthreads; i++) {
-    l1_job *jb = &jobs[i];
-    jb->bits = bits; jb->p = p; jb->b = b; jb->a = a;
-    jb->bytes = bytes; jb->len = len; jb->T = T; jb->y = y;
-    jb->c_begin = n1 * (uint64_t)i / (uint64_t)nthreads;
-    jb->c_end = n1 * (uint64_t)(i + 1) / (uint64_t)nthreads;
-    if (nthreads == 1) l1_worker(jb);
-    else pthread_create(&th[i], NULL, l1_worker, jb);
-  }
-  if (nthreads > 1)
+  if (nthreads == 1) {
+    l1_worker(&one);
+  } else {
+    l1_job *jobs = (l1_job *)calloc((size_t)nthreads, sizeof(l1_job));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    for (int i = 0; i < nthreads; i++) {
+      jobs[i] = one;
+      jobs[i].c_begin = n1 * (uint64_t)i / (uint64_t)nthreads;
+      jobs[i].c_end = n1 * (uint64_t)(i + 1) / (uint64_t)nthreads;
+      pthread_create(&th[i], NULL, l1_worker, &jobs[i]);
+    }
     for (int i = 0; i < nthreads; i++) pthread_join(th[i], NULL);
-  free(jobs);
-  free(th);
+    free(jobs);
+    free(th);
+  }
   int lv = alg1_loop(p, PMPO_M, PMPO_L, 1, b, a, &y, n1, V); /* levels 2.. */
   free(y);
   return lv < 0 ? -1 : lv + 1;

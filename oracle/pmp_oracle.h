@@ -42,6 +42,12 @@ int pmpo_params(int bits, uint64_t *p_lo, uint64_t *p_hi, uint64_t *k,
  * b: 8 words, a: 8*128 words (level-major).  Returns 0, -1 on bad width. */
 int pmpo_keygen(uint64_t seed, int bits, uint64_t *b, uint64_t *a);
 
+/* The generator streams of that contract, for pinning against published
+ * reference outputs: n successive splitmix64 outputs from `state`, and n
+ * successive xoshiro256** outputs from the state s[4] (s is not modified). */
+void pmpo_splitmix64_stream(uint64_t state, uint64_t n, uint64_t *out);
+void pmpo_xoshiro256ss_stream(const uint64_t s[4], uint64_t n, uint64_t *out);
+
 /* Mixing finalizer, P:722-734 (64-bit: 33 / 0xc4ceb9fe1a85ec53 / 33;
  * 32-bit: 13 / 0xab3be54f / 16) and its inverse ("invertible"). */
 uint64_t pmpo_mix(int bits, uint64_t z);

@@ -56,6 +56,7 @@ def lib() -> ctypes.CDLL:
             "pmp_hash_batch_multi": ([_vp, _int, _vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash2_batch_multi": ([_vp, _int, _vp, _vp, _u64, _vp, _vp], _int),
             "pmp_hash_long": ([_vp, _vp, _u64, _vp, _vp], _int),
+            "pmp_hash_long_host": ([_vp, _vp, _u64, _vp, _u64, _vp], _int),
             "pmp_hash_long_partial": ([_vp, _vp, _u64, _u64, _u64, _vp, _vp], _int),
             "pmp_hash_long_combine": ([_vp, _vp, _int, _u64, _vp, _vp], _int),
             "pmp_long_split": ([_int, _u64, _int, _vp], _int),
@@ -71,6 +72,7 @@ def lib() -> ctypes.CDLL:
             "pmp_long_constant": ([_vp, _u64, _vp], _int),
             "pmp_selftest": ([_int, _int, _vp, _u64, _vp, _vp], _int),
             "pmp_launch_count": ([], _u64),
+            "pmp_set_small_batch_max": ([_u64], _u64),
             "pmp_prof_enable": ([_int], None),
             "pmp_prof_reset": ([], None),
             "pmp_prof_read": ([ctypes.c_char_p, _vp, _vp], _int),
@@ -222,6 +224,10 @@ def pmp_launch_count() -> int:
     return int(lib().pmp_launch_count())
 
 
+def pmp_set_small_batch_max(n: int) -> int:
+    return int(lib().pmp_set_small_batch_max(n))
+
+
 def pmp_prof_enable(on: bool) -> None:
     lib().pmp_prof_enable(1 if on else 0)
 
@@ -357,6 +363,25 @@ def hash_batch_host(keys: list, payload, offsets, outs=None, piece_bytes: int = 
                                [ptr(o) for o in outs], piece_bytes, int(st.cuda_stream)), "pmp_hash_batch_host")
     st.synchronize()
     return outs
+
+
+def hash_long_host(keys: Keys, data, piece_bytes: int = 0) -> int:
+    """One host-resident string (numpy uint8 array, bytes, or a pinned torch CPU
+    tensor) streamed through the device (pmp_hash_long_host); returns the
+    digest as a Python int."""
+    import numpy as np
+    import torch
+
+    if isinstance(data, (bytes, bytearray)):
+        data = np.frombuffer(bytes(data), dtype=np.uint8)
+    n = data.numel() if hasattr(data, "numel") else data.size
+    p = data.data_ptr() if hasattr(data, "data_ptr") else (data.ctypes.data if n else 0)
+    out = np.zeros(1, dtype=np.uint64 if keys.bits == 64 else np.uint32)
+    st = torch.cuda.current_stream()
+    _check(lib().pmp_hash_long_host(keys.handle, p, n, out.ctypes.data, piece_bytes, int(st.cuda_stream)),
+           "pmp_hash_long_host")
+    st.synchronize()
+    return int(out[0])
 
 
 def hash_batch_buckets(keys: Keys, payload, offsets, M: int, counts=None, out=None, stream=None):

@@ -28,7 +28,10 @@ struct pmp_keys {
   uint64_t b[kL];
   uint64_t a[kL * kM];
   int device;       // -1: host-only handle
-  uint64_t *d_blob; // device: b[8] then a[8*128]
+  uint64_t *d_blob; // device: b[8] then a[8*128], then the two-level variant's power tables
+  // the power tables are built on first use of the two-level variant (ensure_poly)
+  mutable std::atomic<int> poly_ready{0};
+  mutable std::mutex poly_mu;
 };
 
 namespace {
@@ -63,6 +66,10 @@ uint64_t amax_of(int bits) {  // p - kappa - 1
 }
 u128 prime_of(int bits) { return bits == 64 ? (((u128)1 << 64) + 13) : (((u128)1 << 32) + 15); }
 
+// A private non-blocking stream per device for key uploads and one-time table
+// setup, so that creating a handle never synchronises the whole device.
+cudaStream_t util_stream(int dev);
+
 int upload(pmp_keys *k) {
   k->device = -1;
   k->d_blob = nullptr;
@@ -73,24 +80,43 @@ int upload(pmp_keys *k) {
   }
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return PMP_ECUDA;
-  std::vector<uint64_t> blob(kBlobWords, 0);  // b, a, then the variant's power tables (pmp_poly.cuh)
+  std::vector<uint64_t> blob(kL + kL * kM);  // b, a (the variant's tables follow, built lazily)
   memcpy(blob.data(), k->b, sizeof(k->b));
   memcpy(blob.data() + kL, k->a, sizeof(k->a));
-  if (cudaMalloc(&k->d_blob, blob.size() * 8) != cudaSuccess) return PMP_ENOMEM;
-  if (cudaMemcpy(k->d_blob, blob.data(), blob.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+  if (cudaMalloc(&k->d_blob, (size_t)kBlobWords * 8) != cudaSuccess) return PMP_ENOMEM;
+  cudaStream_t us = util_stream(dev);
+  if (!us || cudaMemcpyAsync(k->d_blob, blob.data(), blob.size() * 8, cudaMemcpyHostToDevice, us) != cudaSuccess ||
+      cudaStreamSynchronize(us) != cudaSuccess) {
     cudaFree(k->d_blob);
     k->d_blob = nullptr;
     return PMP_ECUDA;
   }
-  if (k->bits == 64) k_poly_setup<64><<<1, 32>>>(k->d_blob);
-  else k_poly_setup<32><<<1, 32>>>(k->d_blob);
-  if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
-    cudaFree(k->d_blob);
-    k->d_blob = nullptr;
-    return PMP_ECUDA;
-  }
+  k->poly_ready.store(0);
   k->device = dev;
   return 0;
+}
+
+// The two-level variant's power tables W[i] = r^(128-i) and the ladder R^(2^k)
+// (pmp_poly.cuh), built once per handle before its first two-level call.
+int ensure_poly(const pmp_keys *k) {
+  if (k->poly_ready.load(std::memory_order_acquire)) return 0;
+  std::lock_guard<std::mutex> lk(k->poly_mu);
+  if (k->poly_ready.load(std::memory_order_relaxed)) return 0;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != k->device) cudaSetDevice(k->device);
+  cudaStream_t us = util_stream(k->device);
+  int rc = 0;
+  if (!us) {
+    rc = PMP_ECUDA;
+  } else {
+    if (k->bits == 64) k_poly_setup<64><<<1, 32, 0, us>>>(k->d_blob);
+    else k_poly_setup<32><<<1, 32, 0, us>>>(k->d_blob);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(us) != cudaSuccess) rc = PMP_ECUDA;
+  }
+  if (cur != k->device) cudaSetDevice(cur);
+  if (!rc) k->poly_ready.store(1, std::memory_order_release);
+  return rc;
 }
 
 // ----------------------------------------------------------------- device info
@@ -100,6 +126,20 @@ struct DevInfo {
 };
 std::mutex g_mu;
 DevInfo g_dev[64];
+
+cudaStream_t util_stream(int dev) {
+  static cudaStream_t us[64] = {};
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!us[dev]) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != dev) cudaSetDevice(dev);
+    if (cudaStreamCreateWithFlags(&us[dev], cudaStreamNonBlocking) != cudaSuccess) us[dev] = nullptr;
+    if (cur != dev) cudaSetDevice(cur);
+  }
+  return us[dev];
+}
 
 int sm_count(int dev) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -122,6 +162,7 @@ int sm_count(int dev) {
 
 // ----------------------------------------------------------------- instrumentation
 std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t> g_small_max{kSmallMax};  // batches of <= this many strings take k_small
 std::atomic<int> g_prof{0};
 struct ProfRec {
   std::string name;
@@ -230,7 +271,11 @@ int long_partial_impl(const pmp_keys *k, const uint8_t *local, uint64_t local_le
   s.avail_end = g0 + local_len;
   s.B = total;
   s.delta = (uint32_t)((uintptr_t)local & 15);
-  const bool owns_tail = g0 + local_len == total;
+  // The tail block (the one holding the marker word) belongs to the one
+  // range that holds the last byte, total - 1, so an empty range never owns it
+  // (several empty ranges may end at `total`).  For total == 0 no range owns
+  // it: the whole value is sigma_0 = 1 (reading Q2), added by the combine.
+  const bool owns_tail = local_len > 0 && g0 + local_len == total;
   const uint64_t cb = g0 / CB;
   const uint64_t ce = owns_tail ? gm.T[1] : (g0 + local_len) / CB;
   const int sms = sm_count(k->device);
@@ -303,7 +348,10 @@ int poly_long_impl(const pmp_keys *k, const uint8_t *local, uint64_t local_len, 
   s.avail_end = g0 + local_len;
   s.B = total;
   s.delta = (uint32_t)((uintptr_t)local & 15);
-  const bool owns_tail = g0 + local_len == total;
+  // tail chunk: owned by the range holding byte total - 1; the empty message
+  // (total == 0) has no such range, so there the caller passing g0 == 0 owns
+  // it -- a split of the empty message must be a single range (pmp.h)
+  const bool owns_tail = g0 + local_len == total && (local_len > 0 || total == 0);
   const uint64_t cb = g0 / CB;
   const uint64_t ce = owns_tail ? C : (g0 + local_len) / CB;
   const int sms = sm_count(k->device);
@@ -335,7 +383,8 @@ int poly_args(const pmp_keys *k, const uint8_t *local, uint64_t local_len, uint6
   const uint64_t CB = (uint64_t)chunk_bytes(k->bits);
   if (g0 % CB != 0 || g0 + local_len > total || g0 + local_len < g0) return PMP_EINVAL;
   if (g0 + local_len != total && local_len % CB != 0) return PMP_EINVAL;
-  return check_keys(k);
+  if (int rc = check_keys(k)) return rc;
+  return ensure_poly(k);
 }
 
 }  // namespace
@@ -669,13 +718,12 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   const bool dual = k2 != nullptr;
   if (dual && (!os2 || !os2->out || k->bits != 64 || k2->bits != 32 || k2->device != k->device))
     return PMP_EINVAL;
+  if (v2) {
+    if (int rc = ensure_poly(k)) return rc;
+    if (dual)
+      if (int rc = ensure_poly(k2)) return rc;
+  }
   const int sms = sm_count(k->device);
-  Scratch sc(st), sc_off(st);
-  // work list (n u32) + counters [mid, big, then per schedule: next big, next mid batch; k_short tile claims]
-  if (sc.alloc((size_t)n * 4 + 32)) return PMP_ENOMEM;
-  uint32_t *wcount = (uint32_t *)sc.p;
-  uint32_t *wlist = wcount + 8;
-  if (cudaMemsetAsync(wcount, 0, 28, st) != cudaSuccess) return PMP_ECUDA;
   ParamKeys pk = param_keys(k);
   if (dual) {
     for (int i = 0; i < 32; i++) pk.a32[i] = (uint32_t)k2->a[i];
@@ -683,6 +731,23 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     pk.r32 = k2->a[kM];   // a_{2,1}
     pk.b2_32 = k2->b[1];
   }
+  if (!v2 && n <= g_small_max.load(std::memory_order_relaxed)) {
+    // latency path: one launch, no scratch, no work list (pmp_small.cuh)
+    const unsigned grid = (unsigned)((n + kSmallThreads - 1) / kSmallThreads);
+    const uint64_t *b1 = k->d_blob, *b2 = dual ? k2->d_blob : k->d_blob;
+    const OutSpec o2 = dual ? *os2 : os;
+    return launch("k_small", st, [&] {
+      if (dual) k_small<64, true><<<grid, kSmallThreads, 0, st>>>(pk, b1, b2, bytes, offsets, n, os, o2);
+      else if (k->bits == 64) k_small<64, false><<<grid, kSmallThreads, 0, st>>>(pk, b1, b2, bytes, offsets, n, os, o2);
+      else k_small<32, false><<<grid, kSmallThreads, 0, st>>>(pk, b1, b2, bytes, offsets, n, os, o2);
+    });
+  }
+  Scratch sc(st), sc_off(st);
+  // work list (n u32) + counters [mid, big, then per schedule: next big, next mid batch; k_short tile claims]
+  if (sc.alloc((size_t)n * 4 + 32)) return PMP_ENOMEM;
+  uint32_t *wcount = (uint32_t *)sc.p;
+  uint32_t *wlist = wcount + 8;
+  if (cudaMemsetAsync(wcount, 0, 28, st) != cudaSuccess) return PMP_ECUDA;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
     const void *fs[6] = {(const void *)k_short<64>, (const void *)k_short<32>, (const void *)k_short<64, true>,
@@ -886,6 +951,17 @@ int pmp_hash_batch_host(const pmp_keys *const *keys, int nkeys, const uint8_t *b
     max_span = std::max(max_span, offsets[s1] - offsets[s0]);
     max_cnt = std::max(max_cnt, s1 - s0);
   }
+  // everything below runs on the keys' device (its streams, its memory pool,
+  // its kernels); the caller's current device is restored on return
+  int cur_dev = 0;
+  if (cudaGetDevice(&cur_dev) != cudaSuccess) return PMP_ECUDA;
+  struct DevGuard {
+    int prev, now;
+    ~DevGuard() {
+      if (prev != now) cudaSetDevice(prev);
+    }
+  } guard{cur_dev, dev};
+  if (cur_dev != dev && cudaSetDevice(dev) != cudaSuccess) return PMP_ECUDA;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_host_st[dev].init) {
@@ -945,6 +1021,90 @@ int pmp_hash_batch_host(const pmp_keys *const *keys, int nkeys, const uint8_t *b
   return rc;
 }
 
+int pmp_hash_long_host(const pmp_keys *k, const uint8_t *bytes, uint64_t len, void *out_host, uint64_t piece_bytes,
+                       cudaStream_t stream) {
+  if (!k || !out_host || (!bytes && len > 0)) return PMP_EINVAL;
+  if (int rc = check_keys(k)) return rc;
+  if (words_of(k->bits, len) > (1ULL << 56)) return PMP_ETOOLONG;
+  const int dev = k->device;
+  if (dev < 0 || dev >= 64) return PMP_EINVAL;
+  const uint64_t CB = (uint64_t)chunk_bytes(k->bits);
+  if (piece_bytes == 0) piece_bytes = 256ull << 20;
+  piece_bytes = piece_bytes < CB ? CB : piece_bytes - piece_bytes % CB;
+  int cur_dev = 0;
+  if (cudaGetDevice(&cur_dev) != cudaSuccess) return PMP_ECUDA;
+  struct DevGuard {
+    int prev, now;
+    ~DevGuard() {
+      if (prev != now) cudaSetDevice(prev);
+    }
+  } guard{cur_dev, dev};
+  if (cur_dev != dev && cudaSetDevice(dev) != cudaSuccess) return PMP_ECUDA;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_host_st[dev].init) {
+      for (int q = 0; q < kHostSlots; q++) cudaStreamCreateWithFlags(&g_host_st[dev].st[q], cudaStreamNonBlocking);
+      g_host_st[dev].init = true;
+    }
+  }
+  cudaStream_t *cst = g_host_st[dev].st;
+  // incremental state, stream-ordered on `stream` (allocated and released there)
+  pmp_stream s;
+  s.k = k;
+  s.d_state = nullptr;
+  s.d_tail = nullptr;
+  s.d_s2 = nullptr;
+  s.s2_cap = 0;
+  s.tail_len = s.c_done = 0;
+  s.finalized = false;
+  const size_t nslot = len > piece_bytes ? kHostSlots : 1;
+  const size_t slot_bytes = (size_t)(len < piece_bytes ? len : piece_bytes) + 16;
+  uint8_t *slab = nullptr;   // state | tail | digest | slots
+  const size_t st_bytes = (sizeof(StreamState) + 255) & ~(size_t)255;
+  const size_t hdr = st_bytes + (((size_t)CB + 32 + 255) & ~(size_t)255) + 256;
+  if (cudaMallocAsync((void **)&slab, hdr + nslot * ((slot_bytes + 255) & ~(size_t)255), stream) != cudaSuccess)
+    return PMP_ENOMEM;
+  s.d_state = (StreamState *)slab;
+  s.d_tail = slab + st_bytes;
+  uint64_t *d_dig = (uint64_t *)(slab + hdr - 256);
+  uint8_t *slot[kHostSlots];
+  for (size_t q = 0; q < nslot; q++) slot[q] = slab + hdr + q * ((slot_bytes + 255) & ~(size_t)255);
+  int rc = 0;
+  if (cudaMemsetAsync(s.d_state, 0, sizeof(StreamState), stream) != cudaSuccess) rc = PMP_ECUDA;
+  cudaEvent_t ev_start = nullptr, copied[kHostSlots] = {}, consumed[kHostSlots] = {};
+  if (!rc && cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) != cudaSuccess) rc = PMP_ECUDA;
+  for (int q = 0; q < kHostSlots && !rc; q++)
+    if (cudaEventCreateWithFlags(&copied[q], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&consumed[q], cudaEventDisableTiming) != cudaSuccess)
+      rc = PMP_ECUDA;
+  if (!rc) {
+    cudaEventRecord(ev_start, stream);  // the copies start after prior work on `stream` (and the allocation)
+    for (int q = 0; q < kHostSlots; q++) cudaStreamWaitEvent(cst[q], ev_start, 0);
+  }
+  for (uint64_t off = 0, p = 0; off < len && !rc; off += piece_bytes, p++) {
+    const int q = (int)(p % nslot);
+    const uint64_t sz = len - off < piece_bytes ? len - off : piece_bytes;
+    if (p >= nslot) cudaStreamWaitEvent(cst[q], consumed[q], 0);   // the slot's previous piece is hashed
+    if (cudaMemcpyAsync(slot[q], bytes + off, sz, cudaMemcpyHostToDevice, cst[q]) != cudaSuccess) rc = PMP_ECUDA;
+    cudaEventRecord(copied[q], cst[q]);
+    cudaStreamWaitEvent(stream, copied[q], 0);
+    if (!rc) rc = k->bits == 64 ? stream_update<64>(&s, slot[q], sz, stream) : stream_update<32>(&s, slot[q], sz, stream);
+    cudaEventRecord(consumed[q], stream);
+  }
+  if (!rc) rc = k->bits == 64 ? stream_final<64>(&s, d_dig, stream) : stream_final<32>(&s, d_dig, stream);
+  if (!rc && cudaMemcpyAsync(out_host, d_dig, (size_t)k->bits / 8, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+    rc = PMP_ECUDA;
+  if (s.d_s2) cudaFreeAsync(s.d_s2, stream);
+  cudaFreeAsync(slab, stream);
+  if (ev_start) cudaEventDestroy(ev_start);
+  for (int q = 0; q < kHostSlots; q++) {
+    if (copied[q]) cudaEventDestroy(copied[q]);
+    if (consumed[q]) cudaEventDestroy(consumed[q]);
+  }
+  if (!rc && cudaGetLastError() != cudaSuccess) rc = PMP_ECUDA;
+  return rc;
+}
+
 int pmp_hash_long_partial(const pmp_keys *k, const uint8_t *local, uint64_t local_len, uint64_t g0,
                           uint64_t total, uint64_t *partial, cudaStream_t st) {
   if (!k || !partial || (!local && local_len > 0)) return PMP_EINVAL;
@@ -961,7 +1121,9 @@ int pmp_hash_long_combine(const pmp_keys *k, const uint64_t *partials, int G, ui
                           void *out, cudaStream_t st) {
   if (!k || !partials || !out || G < 1) return PMP_EINVAL;
   if (int rc = check_keys(k)) return rc;
-  const u128 c = long_constant(k, total);
+  // key-only part of V; for the empty message the whole value, sigma_0 = 1
+  // (no range owns a tail there, see long_partial_impl)
+  const u128 c = total == 0 ? (u128)1 : long_constant(k, total);
   const uint64_t clo = (uint64_t)c, chi = (uint64_t)(c >> 64);
   if (k->bits == 64)
     return launch("k_combine", st, [&] { k_combine<64><<<1, 32, 0, st>>>(partials, G, clo, chi, out); });
@@ -1006,6 +1168,7 @@ int pmp_hash2_long_partial(const pmp_keys *k, const uint8_t *local, uint64_t loc
 int pmp_hash2_long_combine(const pmp_keys *k, const uint64_t *partials, int G, void *out, cudaStream_t st) {
   if (!k || !partials || !out || G < 1) return PMP_EINVAL;
   if (int rc = check_keys(k)) return rc;
+  if (int rc = ensure_poly(k)) return rc;
   if (k->bits == 64)
     return launch("k_poly_sum", st, [&] { k_poly_sum<64><<<1, 256, 0, st>>>(k->d_blob, partials, (uint64_t)G, 1, out); });
   return launch("k_poly_sum", st, [&] { k_poly_sum<32><<<1, 256, 0, st>>>(k->d_blob, partials, (uint64_t)G, 1, out); });
@@ -1040,6 +1203,8 @@ int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_
 }
 
 uint64_t pmp_launch_count(void) { return g_launches.load(); }
+
+uint64_t pmp_set_small_batch_max(uint64_t n) { return g_small_max.exchange(n); }
 
 void pmp_prof_enable(int on) { g_prof.store(on ? 1 : 0); }
 

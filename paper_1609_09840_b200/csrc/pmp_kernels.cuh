@@ -15,6 +15,7 @@
 //                    parallel over level-2 nodes, split across callers
 //   pmp_stream.cuh   incremental hashing with device-resident level state
 //   pmp_misc.cuh     self-test hooks, the hash-table histogram pass
+//   pmp_small.cuh    k_small: the latency path for small batches (one launch)
 //   pmp_poly.cuh     (included by pmp_api.cu) long strings, two-level variant
 //
 // Citations: P:n = PAPER.md line n.  Eq. (1); Algorithm 1 P:427-443;
@@ -27,3 +28,4 @@
 #include "pmp_long.cuh"
 #include "pmp_stream.cuh"
 #include "pmp_misc.cuh"
+#include "pmp_small.cuh"

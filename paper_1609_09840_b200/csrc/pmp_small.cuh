@@ -1,0 +1,133 @@
+// pmp_small.cuh -- latency path for small batches (k_small): one launch, no scratch
+// (part of the kernels included by pmp_kernels.cuh; citations as there)
+#pragma once
+#include "pmp_engine.cuh"
+#include "pmp_short.cuh"
+
+namespace pmp {
+
+// ============================================================= k_small
+// A batch of n <= kSmallMax strings in ONE launch with no scratch memory and
+// no host-side work besides the launch: the throughput path (k_short's TMA
+// pipeline, a zeroed work list, k_wstring) costs ~20 us of fixed latency that
+// dominates a call of a few thousand strings (BASELINE configs[0]: 1,000).
+//   - one thread per string; a string of <= kShortMax bytes is hashed straight
+//     from global memory by the same word loop as k_short (short_tree_lo /
+//     short_tree_dual, the `direct` fetch: aligned 32-bit loads of the words
+//     overlapping the string, never past its end);
+//   - longer strings are listed in shared memory and hashed afterwards by the
+//     block's warps, one warp per string: level-2 nodes by the warp chunk
+//     engine (warp_chunks), levels >= 3 streamed bottom-up.
+constexpr int kSmallThreads = 256;
+constexpr uint64_t kSmallMax = 4096;   // strings per call routed here (pmp_api.cu)
+
+// V mod 2^n of one string of B > kShortMax bytes hashed by one warp (every
+// lane returns the value).  Keys from the device blob (b[8], a[8][128]).
+template <int BITS>
+__device__ __noinline__ uint64_t warp_hash_string(const uint64_t *__restrict__ blob, const uint8_t *sa, uint64_t B,
+                                                  int lane) {
+  using Fe = typename Tr<BITS>::Fe;
+  using Acc = typename Tr<BITS>::Acc;
+  const uint64_t *bk = blob, *ak = blob + kL;
+  const Geom gm = make_geom(B / Tr<BITS>::W + 1);
+  StrView s;
+  s.base = sa;
+  s.g0 = 0;
+  s.avail_end = B;
+  s.B = B;
+  s.delta = (uint32_t)((uintptr_t)sa & 15);
+  LaneKeys<BITS> lk;
+  lk.load(ak, lane & 7);
+  if (gm.leff <= 1) {          // one level-1 block: its value is the tree value
+    const ChunkOut<BITS> co = warp_chunks<BITS>(s, 0, 1, lk, bk[0], ak + kM, lane);
+    return fe_lo(co.v1_first);
+  }
+  // levels 3..leff: the open node's exact running sum and child count per level
+  Acc up[kL + 1];
+  uint64_t cnt[kL + 1];
+#pragma unroll
+  for (int j = 0; j <= (int)kL; j++) {
+    acc_zero(up[j]);
+    cnt[j] = 0;
+  }
+  Fe root = Fe();
+  for (uint64_t q = 0; q < gm.T[2]; q++) {
+    const uint64_t ce = min(128 * q + 128, gm.T[1]);
+    ChunkOut<BITS> co = warp_chunks<BITS, false, true>(s, 128 * q, ce, lk, bk[0], ak + kM, lane);
+    acc_add_word(co.acc2, bk[1]);                       // b_2 + sum_r a_{2,r} v_1 (Eq. (1))
+    Fe v = acc_reduce(co.acc2);
+    // push v up: level j receives child cnt[j] of its open node
+    for (int j = 3; j <= gm.leff; j++) {
+      acc_mac_fe(up[j], ak[(uint64_t)(j - 1) * kM + (cnt[j] & 127)], v);
+      cnt[j]++;
+      if ((cnt[j] & 127) != 0 && cnt[j] != gm.T[j - 1]) break;   // node still open
+      acc_add_word(up[j], bk[j - 1]);
+      v = acc_reduce(up[j]);
+      acc_zero(up[j]);
+    }
+    if (gm.leff == 2 || (q + 1 == gm.T[2])) root = v;  // the last close reaches the root
+  }
+  return fe_lo(root);
+}
+
+template <int BITS, bool DUAL>
+__global__ void __launch_bounds__(kSmallThreads)
+k_small(const ParamKeys K, const uint64_t *__restrict__ blob, const uint64_t *__restrict__ blob32,
+        const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets, uint64_t n, const OutSpec os,
+        const OutSpec os2) {
+  __shared__ uint64_t skeys[32];
+  __shared__ uint32_t skeys32[32];
+  __shared__ uint32_t longs[kSmallThreads];
+  __shared__ uint32_t nlong;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    skeys[threadIdx.x] = K.a[threadIdx.x];
+    if (DUAL) skeys32[threadIdx.x] = K.a32[threadIdx.x];
+  }
+  if (threadIdx.x == 0) nlong = 0;
+  __syncthreads();
+  const uint64_t i = (uint64_t)blockIdx.x * kSmallThreads + threadIdx.x;
+  const bool valid = i < n;
+  const uint64_t o0 = valid ? offsets[i] : 0, B64 = valid ? offsets[i + 1] - o0 : 0;
+  const bool is_short = valid && B64 <= kShortMax;
+  if (valid && !is_short) longs[atomicAdd(&nlong, 1u)] = (uint32_t)i;
+  const uint32_t B = is_short ? (uint32_t)B64 : 0u;
+  const int tfm = (int)__reduce_max_sync(FULL, B / (BITS / 8));
+  if (is_short) {
+    const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
+    const uintptr_t pa = sa & ~(uintptr_t)3;
+    auto fetch = [&](int kk) {
+      const uintptr_t a = pa + 4 * (uintptr_t)kk;
+      return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
+    };
+    const uint32_t sh = 8 * (uint32_t)(sa & 3);
+    if constexpr (DUAL) {
+      uint64_t lo;
+      uint32_t lo32;
+      short_tree_dual<false>(K, skeys, skeys32, B, sh, tfm, fetch, lo, lo32);
+      emit<64>(os, i, lo);
+      emit<32>(os2, i, lo32);
+    } else {
+      emit<BITS>(os, i, short_tree_lo<BITS, false>(K, skeys, B, sh, tfm, fetch));
+    }
+  }
+  __syncthreads();
+  const int nw = kSmallThreads / 32;
+  for (uint32_t j = threadIdx.x >> 5; j < nlong; j += nw) {
+    const uint32_t si = longs[j];
+    const uint64_t a0 = offsets[si], len = offsets[si + 1] - a0;
+    if constexpr (DUAL) {
+      const uint64_t lo = warp_hash_string<64>(blob, bytes + a0, len, lane);
+      const uint64_t lo32 = warp_hash_string<32>(blob32, bytes + a0, len, lane);
+      if (lane == 0) {
+        emit<64>(os, si, lo);
+        emit<32>(os2, si, lo32);
+      }
+    } else {
+      const uint64_t lo = warp_hash_string<BITS>(blob, bytes + a0, len, lane);
+      if (lane == 0) emit<BITS>(os, si, lo);
+    }
+  }
+}
+
+}  // namespace pmp

@@ -55,27 +55,49 @@ def long_ranges(bits: int, total_len: int, world: int) -> list[tuple[int, int]]:
     return [(b[g], b[g + 1]) for g in range(world)]
 
 
+def gather_partials(mine, world: int, group=None):
+    """All-gather the 16-byte partials of every rank into one (2*world,) int64
+    tensor on ``mine``'s device, on the current stream.  NCCL: one
+    all_gather_into_tensor of device buffers.  Other backends (gloo, the CPU
+    test path): the partial is staged through host memory."""
+    import torch
+    import torch.distributed as dist
+
+    parts = torch.zeros(2 * world, dtype=torch.int64, device=mine.device)
+    if world == 1:
+        parts.copy_(mine)
+        return parts
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(parts, mine, group=group)
+        return parts
+    host = mine.cpu()
+    lst = [torch.zeros_like(host) for _ in range(world)]
+    dist.all_gather(lst, host, group=group)
+    parts.copy_(torch.cat(lst))
+    return parts
+
+
 def hash_long_distributed(keys: Keys, local, local_len: int, global_offset: int, total_len: int,
                           group=None, stream=None):
-    """Partial on this rank's GPU -> all_gather of the 16-byte partials (NCCL) ->
-    combine.  ``local`` is a uint8 CUDA tensor holding this rank's bytes.
-    Returns the digest tensor (1 element) on every rank."""
+    """Partial on this rank's GPU -> all_gather of the 16-byte partials (NCCL,
+    or host-staged for gloo) -> combine.  ``local`` is a uint8 CUDA tensor
+    holding this rank's bytes [global_offset, global_offset + local_len).
+    Every step (the partial kernel, the collective, the combine) is ordered on
+    ``stream`` (default: the current stream).  Returns the digest tensor
+    (1 element) on every rank."""
+    import contextlib
+
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    dev = local.device
-    mine = torch.zeros(2, dtype=torch.int64, device=dev)
-    sp = _stream_ptr(stream)
-    _check(pmp_hash_long_partial(keys.handle, local.data_ptr(), local_len, global_offset, total_len,
-                                 mine.data_ptr(), sp), "pmp_hash_long_partial")
-    parts = torch.zeros(2 * world, dtype=torch.int64, device=dev)
-    if world > 1:
-        dist.all_gather_into_tensor(parts, mine, group=group)
-    else:
-        parts.copy_(mine)
-    out = torch.empty(1, dtype=torch.int64 if keys.bits == 64 else torch.int32, device=dev)
-    _check(pmp_hash_long_combine(keys.handle, parts.data_ptr(), world, total_len, out.data_ptr(), sp),
-           "pmp_hash_long_combine")
+    with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+        sp = _stream_ptr(None)
+        mine = torch.zeros(2, dtype=torch.int64, device=local.device)
+        _check(pmp_hash_long_partial(keys.handle, local.data_ptr(), local_len, global_offset, total_len,
+                                     mine.data_ptr(), sp), "pmp_hash_long_partial")
+        parts = gather_partials(mine, world, group)
+        out = torch.empty(1, dtype=torch.int64 if keys.bits == 64 else torch.int32, device=local.device)
+        _check(pmp_hash_long_combine(keys.handle, parts.data_ptr(), world, total_len, out.data_ptr(), sp),
+               "pmp_hash_long_combine")
     return out

@@ -29,6 +29,15 @@ def torch_dev():
     return torch.device("cuda:0")
 
 
+@pytest.fixture(params=["throughput", "latency"])
+def batch_path(request, torch_dev):
+    """Run a batch test through the throughput path (k_short + k_wstring) and
+    through the latency path (k_small, batches of <= 4096 strings)."""
+    prev = pmp.pmp_set_small_batch_max(0 if request.param == "throughput" else 4096)
+    yield request.param
+    pmp.pmp_set_small_batch_max(prev)
+
+
 def _u(bits):
     return np.uint64 if bits == 64 else np.uint32
 
@@ -131,6 +140,7 @@ def test_mixer_matches_oracle(torch_dev, oracle_lib, bits):
 
 # ------------------------------------------------------------ batch path
 @pytest.mark.parametrize("bits", [32, 64])
+@pytest.mark.usefixtures("batch_path")
 def test_tiny_config_every_hash(torch_dev, oracle_lib, bits):
     """configs[0] (1,000 strings, U[1,64] B, seed 1), every digest; at 32 bits too."""
     wl = datagen.WORKLOADS["tiny"]
@@ -156,6 +166,7 @@ def test_keyfile_schedule_hashes_like_generated(torch_dev, oracle_lib, bits):
 
 @pytest.mark.parametrize("bits", [32, 64])
 @pytest.mark.parametrize("shift", [0, 1, 3, 8, 13])
+@pytest.mark.usefixtures("batch_path")
 def test_length_sweep_all_paths(torch_dev, oracle_lib, bits, shift):
     """Every length 0..2100 (short path <= 127 B, warp path beyond, 1..3 level-1
     blocks, ragged tails, marker-only blocks), payload shifted by `shift` bytes."""
@@ -172,6 +183,7 @@ def test_length_sweep_all_paths(torch_dev, oracle_lib, bits, shift):
 
 
 @pytest.mark.parametrize("bits", [32, 64])
+@pytest.mark.usefixtures("batch_path")
 def test_all_short_batch_alignments(torch_dev, oracle_lib, bits):
     """The staged all-short warp path with every start alignment and empty strings."""
     rng = np.random.default_rng(bits + 100)
@@ -185,6 +197,7 @@ def test_all_short_batch_alignments(torch_dev, oracle_lib, bits):
 
 @pytest.mark.parametrize("bits", [32, 64])
 @pytest.mark.parametrize("shift", [0, 5])
+@pytest.mark.usefixtures("batch_path")
 def test_mid_strings_group_path(torch_dev, oracle_lib, bits, shift):
     """Mid strings (128 B <= B < 64 KiB: one 8-lane group per string, four per
     warp, warp batches of 32 handed out as groups finish): lengths at and around
@@ -208,6 +221,7 @@ def test_mid_strings_group_path(torch_dev, oracle_lib, bits, shift):
 
 
 @pytest.mark.parametrize("bits", [32, 64])
+@pytest.mark.usefixtures("batch_path")
 def test_long_strings_in_batch(torch_dev, oracle_lib, bits):
     """Warp-per-string path across level-2 (128 blocks) and level-3 (128^2 blocks)
     boundaries, misaligned starts, mixed with short strings and big ones first."""
@@ -224,6 +238,7 @@ def test_long_strings_in_batch(torch_dev, oracle_lib, bits):
 
 
 @pytest.mark.parametrize("bits", [32, 64])
+@pytest.mark.usefixtures("batch_path")
 def test_algorithm2_rare_branches_end_to_end(torch_dev, oracle_lib, bits):
     """Key schedules built so a block sum equals 2^n - j (v1 = 2 branch of
     Algorithm 2) or 2^n (v1 = 1 branch): b = 2^n - 2 - j, a = 1, one data word 1
@@ -296,9 +311,45 @@ def test_long_partition_invariance(torch_dev, oracle_lib, bits):
         assert got == ref, b
 
 
+@pytest.mark.parametrize("bits", [32, 64])
+def test_long_partition_degenerate_ranges(torch_dev, oracle_lib, bits):
+    """Splits with empty ranges: the tail block belongs to the range
+    holding the last byte only, so pmp_long_split(total, G) for tiny totals,
+    trailing / leading / repeated empty ranges, and the empty message give the
+    one-call digest (= the oracle's) for every G."""
+    import torch
+
+    cb = 128 * bits // 8
+    keys = pmp.Keys.generate(9, bits)
+    okeys = oracle_lib.keygen(9, bits)
+    for total in (0, 1, 3, 5, cb - 1, cb, 2 * cb, 3 * cb + 7, 128 * cb, 128 * cb + 1):
+        data = datagen.payload_host(9, 0, max(total, 1))[:total]
+        d = torch.from_numpy(np.concatenate([data, np.zeros(16, np.uint8)])).to(torch_dev)
+        want = oracle_lib.hash_long(okeys, data, nthreads=NT)
+        assert int(pmp.as_u64(pmp.hash_long(keys, d, total))[0]) == want, total
+        splits = [pmp.pmp_long_split(bits, total, G) for G in (1, 2, 3, 8)]
+        nb = total // cb
+        splits += [[0, 0, total], [0, 0, 0, total]]
+        if total % cb == 0:                   # a range may start at `total` only if block-aligned
+            splits += [[0, total, total], [0, 0, total, total, total]]
+            if nb >= 2:
+                splits += [[0, cb, total, total]]
+        if nb >= 2:
+            splits += [[0, cb, cb, total]]
+        for b in splits:
+            G = len(b) - 1
+            parts = torch.zeros(2 * G, dtype=torch.int64, device=torch_dev)
+            for g in range(G):
+                pmp.hash_long_partial(keys, d[b[g]:], b[g + 1] - b[g], b[g], total,
+                                      partial=parts[2 * g:2 * g + 2])
+            got = int(pmp.as_u64(pmp.hash_long_combine(keys, parts, total))[0])
+            assert got == want, (total, b)
+
+
 # ------------------------------------------------------------ hash-table consumer (SURVEY 8(f3))
 @pytest.mark.parametrize("bits", [32, 64])
 @pytest.mark.parametrize("M", [1, 7, 1024, 50_000, 2**32 - 1])   # 50,000: histogram without the smem copy
+@pytest.mark.usefixtures("batch_path")
 def test_buckets_and_histogram(torch_dev, oracle_lib, bits, M):
     """pmp_hash_batch_buckets == oracle digest mod M, and its fused histogram ==
     bincount, for a batch mixing short, long, empty and misaligned strings."""
@@ -457,6 +508,7 @@ def test_stream_reset_and_reuse(torch_dev, oracle_lib):
 
 
 @pytest.mark.parametrize("piece", [0, 4096, 100_000])
+@pytest.mark.usefixtures("batch_path")
 def test_host_batch_streaming(torch_dev, oracle_lib, piece):
     """pmp_hash_batch_host (host-resident bytes/offsets/digests, two key
     schedules at once) equals the device path and the oracle: pieces smaller
@@ -474,7 +526,28 @@ def test_host_batch_streaming(torch_dev, oracle_lib, piece):
     assert np.array_equal(got64, run_batch(torch_dev, k64, pay, off))
 
 
+@pytest.mark.parametrize("bits", [32, 64])
+def test_long_host_streaming(torch_dev, oracle_lib, bits):
+    """pmp_hash_long_host (host-resident string -> pieces copied into three device
+    slots on internal streams -> incremental device state): equal to
+    pmp_hash_long and the oracle for lengths around block / node boundaries and
+    piece sizes smaller than, equal to and larger than the string."""
+    import torch
+
+    cb = 128 * bits // 8
+    keys = pmp.Keys.generate(61, bits)
+    ok = oracle_lib.keygen(61, bits)
+    for total in (0, 1, 7, cb - 1, cb, cb + 1, 128 * cb + 5, 3 * 128 * cb + 777):
+        data = datagen.payload_host(61, 0, max(total, 1))[:total]
+        want = oracle_lib.hash_long(ok, data, nthreads=NT)
+        pinned = torch.from_numpy(data.copy()).pin_memory() if total else torch.zeros(0, dtype=torch.uint8)
+        for piece in (0, cb, 3 * cb, 1 << 20):
+            assert pmp.hash_long_host(keys, pinned, piece_bytes=piece) == want, (total, piece)
+        assert pmp.hash_long_host(keys, data, piece_bytes=5 * cb) == want, total   # pageable host memory
+
+
 @pytest.mark.parametrize("order", [(64, 32), (32, 64), (64, 64, 32), (32,)])
+@pytest.mark.usefixtures("batch_path")
 def test_multi_schedule_fused_pass(torch_dev, oracle_lib, order):
     """pmp_hash_batch_multi: a 64-bit and a 32-bit schedule are fused into one
     pass over the short strings (the 32-bit words are the halves of the 64-bit
@@ -503,6 +576,7 @@ def test_multi_schedule_fused_pass(torch_dev, oracle_lib, order):
 
 
 @pytest.mark.parametrize("trial", range(32))
+@pytest.mark.usefixtures("batch_path")
 def test_random_batches_soak(torch_dev, oracle_lib, trial):
     """Randomised batches through every batch entry point (pmp_hash_batch,
     the fused two-schedule pmp_hash_batch_multi, the host-resident path):
@@ -540,6 +614,7 @@ def test_random_batches_soak(torch_dev, oracle_lib, trial):
     assert np.array_equal(h64, want64) and np.array_equal(h32, want32)
 
 
+@pytest.mark.usefixtures("batch_path")
 def test_entry_points_edge_cases(torch_dev, oracle_lib):
     """n = 0 is a no-op and n = 1 works through every batch entry point; an
     offsets array that is not 16-byte aligned (the kernels' TMA source) is

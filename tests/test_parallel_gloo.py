@@ -120,3 +120,87 @@ def test_shard_batch_tiles_and_balances():
         for l, h in rs:
             sub, b0, b1 = parallel.rebase_offsets(off, l, h)
             assert sub[0] == 0 and int(sub[-1]) == b1 - b0
+
+
+def _gpu_worker(rank, world, port, bits, total, seed, q):
+    """One rank on cuda:0: its byte range of the long string through the real
+    pmp_hash_long_partial (parallel.hash_long_distributed: partial kernel ->
+    host-staged gloo all-gather -> combine kernel), and its byte-balanced shard
+    of a batch through pmp_hash_batch (parallel.shard_batch), digests gathered."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import datagen
+        import paper_1609_09840_b200 as pmp
+        from paper_1609_09840_b200 import parallel
+
+        torch.cuda.set_device(0)
+        keys = pmp.Keys.generate(seed, bits)
+        b, e = parallel.long_ranges(bits, total, world)[rank]
+        local = torch.from_numpy(datagen.payload_host(seed, b, e - b)).cuda()
+        side = torch.cuda.Stream()
+        dig = parallel.hash_long_distributed(keys, local, e - b, b, total, stream=side)
+        side.synchronize()
+        long_digest = int(pmp.as_u64(dig)[0])
+        # batch shard (strong scaling: one global batch, byte-balanced ranges)
+        lens = datagen.lengths(datagen.LEN_LOGUNIFORM, seed, 6000, 1, 1 << 16)
+        off = datagen.offsets_from_lengths(lens)
+        lo, hi = parallel.shard_batch(off, world)[rank]
+        sub, b0, b1 = parallel.rebase_offsets(off, lo, hi)
+        pay = torch.from_numpy(datagen.payload_host(seed, b0, b1 - b0)).cuda()
+        out = pmp.hash_batch(keys, pay, torch.from_numpy(sub.view(np.int64)).cuda())
+        mine = torch.from_numpy(pmp.as_u64(out).astype(np.uint64).view(np.int64))
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([mine.numel()], dtype=torch.int64))
+        mx = int(max(s.item() for s in sizes))
+        padded = torch.zeros(mx, dtype=torch.int64)
+        padded[:mine.numel()] = mine
+        lst = [torch.zeros(mx, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(lst, padded)
+        batch = np.concatenate([l[:int(s.item())].numpy() for l, s in zip(lst, sizes)]).view(np.uint64)
+        q.put((rank, long_digest, batch if rank == 0 else None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits,total", [(64, 128 * 128 * 1024 + 3 * 1024 + 77), (32, 128 * 512 * 5 + 13)])
+def test_distributed_long_and_batch_on_gpu(bits, total):
+    """World size 2 (gloo, both ranks on cuda:0 -- the collective is host-staged,
+    so no kernel waits on another rank): the multi-rank long-string split and the
+    strong-scaling batch shard run the real kernels and equal the one-GPU call
+    and the oracle."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import datagen
+    import oracle
+    import paper_1609_09840_b200 as pmp
+
+    world, seed = 2, 23
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, bits, total, seed, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted((q.get(timeout=600) for _ in range(world)), key=lambda x: x[0])
+    for pr in procs:
+        pr.join(timeout=60)
+    ok = oracle.keygen(seed, bits)
+    data = datagen.payload_host(seed, 0, total)
+    want_long = oracle.hash_long(ok, data, nthreads=os.cpu_count() or 4)
+    assert res[0][1] == want_long and res[1][1] == want_long
+    torch.cuda.set_device(0)
+    keys = pmp.Keys.generate(seed, bits)
+    one = int(pmp.as_u64(pmp.hash_long(keys, torch.from_numpy(data).cuda(), total))[0])
+    assert one == want_long
+    lens = datagen.lengths(datagen.LEN_LOGUNIFORM, seed, 6000, 1, 1 << 16)
+    off = datagen.offsets_from_lengths(lens)
+    pay = datagen.payload_host(seed, 0, int(off[-1]))
+    want_batch = oracle.hash_batch(ok, pay, off, nthreads=os.cpu_count() or 4)
+    assert np.array_equal(res[0][2], want_batch.astype(np.uint64) if bits == 64 else want_batch.astype(np.uint32).astype(np.uint64))
