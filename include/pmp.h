@@ -273,6 +273,21 @@ int pmp_long_split(int out_bits, uint64_t total_len, int G, uint64_t *begins);
 /* Host-only helper (test hook): the key-only constant C(total_len) as (lo, hi). */
 int pmp_long_constant(const pmp_keys *keys, uint64_t total_len, uint64_t *c2);
 
+/* Quality suite (SPEC quality_suite collision_monte_carlo):
+ * Monte Carlo over nsched random key schedules, schedule i being
+ * pmp_keygen(seed0 + i, out_bits) (drawn on the device by the same contract),
+ * of a FIXED pair of strings s1, s2 (device, <= 127 bytes each: one level-1
+ * block, so only b_1 and a_{1,0..31} are drawn).  Adds to counts[0..3]
+ * (device, 4 uint64, caller-zeroed) the number of schedules whose digests are
+ * equal in all n bits, in their low 16, 12 and 8 bits.  dig1 / dig2 (device,
+ * nsched uint64 each, or NULL) receive the digests.  Table 3 bounds the
+ * full-digest collision probability of distinct equal-length strings by
+ * eps ~ 2^-60 (PM+64) / 2^-28 (PM+32); s1 == s2 collides always.
+ * PMP_EINVAL for a longer string or a bad width. */
+int pmp_quality_collisions(int out_bits, uint64_t seed0, uint64_t nsched, const uint8_t *s1, uint32_t len1,
+                           const uint8_t *s2, uint32_t len2, uint64_t *dig1, uint64_t *dig2, uint64_t *counts,
+                           struct CUstream_st *stream);
+
 /* Device self-test hooks running the hot path's own device functions:
  * mode 0: in = n triples (w0, w1, w2) -> (w0 + w1 2^n + w2 2^2n) mod p via the
  *         Section 6.2 reduction and Algorithm 2; w2 <= 2^16;

@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
             "pmp_selftest": ([_int, _int, _vp, _u64, _vp, _vp], _int),
             "pmp_launch_count": ([], _u64),
             "pmp_set_small_batch_max": ([_u64], _u64),
+            "pmp_quality_collisions": ([_int, _u64, _u64, _vp, ctypes.c_uint32, _vp, ctypes.c_uint32, _vp, _vp, _vp,
+                                        _vp], _int),
             "pmp_prof_enable": ([_int], None),
             "pmp_prof_reset": ([], None),
             "pmp_prof_read": ([ctypes.c_char_p, _vp, _vp], _int),

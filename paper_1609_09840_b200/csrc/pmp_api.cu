@@ -38,29 +38,6 @@ namespace {
 
 typedef unsigned __int128 u128;
 
-// ----------------------------------------------------------------- keygen
-uint64_t splitmix(uint64_t &s) {
-  uint64_t z = (s += 0x9E3779B97F4A7C15ULL);
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-  return z ^ (z >> 31);
-}
-struct Xoshiro {
-  uint64_t s[4];
-  static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
-  uint64_t next() {
-    const uint64_t result = rotl(s[1] * 5, 7) * 9;
-    const uint64_t t = s[1] << 17;
-    s[2] ^= s[0];
-    s[3] ^= s[1];
-    s[1] ^= s[2];
-    s[0] ^= s[3];
-    s[2] ^= t;
-    s[3] = rotl(s[3], 45);
-    return result;
-  }
-};
-
 uint64_t amax_of(int bits) {  // p - kappa - 1
   return bits == 64 ? 0xFFFFFFFFFFFFFFF4ULL /* 2^64 - 12 */ : 0xFFFFFFF2ULL /* 2^32 - 14 */;
 }
@@ -560,20 +537,11 @@ pmp_keys *pmp_keygen(uint64_t seed, int out_bits) {
   pmp_keys *k = new (std::nothrow) pmp_keys;
   if (!k) return nullptr;
   k->bits = out_bits;
-  uint64_t sm = seed;
-  Xoshiro g;
-  for (int i = 0; i < 4; i++) g.s[i] = splitmix(sm);
-  const uint64_t amax = amax_of(out_bits);
+  KeyStream g;  // the key-generation contract, reading Q12 (pmp_common.cuh)
+  g.init(seed, out_bits);
   for (uint32_t j = 0; j < kL; j++) {
-    uint64_t x = g.next();
-    k->b[j] = out_bits == 64 ? x : (x >> 32);
-    for (uint32_t i = 0; i < kM; i++) {
-      do {
-        x = g.next();
-        if (out_bits == 32) x >>= 32;
-      } while (x == 0 || x > amax);
-      k->a[j * kM + i] = x;
-    }
+    k->b[j] = g.draw_b();
+    for (uint32_t i = 0; i < kM; i++) k->a[j * kM + i] = g.draw_a();
   }
   if (upload(k) != 0) {
     delete k;
@@ -1205,6 +1173,27 @@ int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_
 uint64_t pmp_launch_count(void) { return g_launches.load(); }
 
 uint64_t pmp_set_small_batch_max(uint64_t n) { return g_small_max.exchange(n); }
+
+int pmp_quality_collisions(int out_bits, uint64_t seed0, uint64_t nsched, const uint8_t *s1, uint32_t len1,
+                           const uint8_t *s2, uint32_t len2, uint64_t *dig1, uint64_t *dig2, uint64_t *counts,
+                           cudaStream_t st) {
+  if ((out_bits != 32 && out_bits != 64) || !counts || len1 > kShortMax || len2 > kShortMax ||
+      (len1 && !s1) || (len2 && !s2))
+    return PMP_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return PMP_ENODEV;
+  if (nsched == 0) return 0;
+  const uint64_t grid = (nsched + 255) / 256;
+  if (grid >= (1ull << 31)) return PMP_EINVAL;
+  unsigned long long *c = reinterpret_cast<unsigned long long *>(counts);
+  if (out_bits == 64)
+    return launch("k_collide_mc", st, [&] {
+      k_collide_mc<64><<<(unsigned)grid, 256, 0, st>>>(seed0, nsched, s1, len1, s2, len2, dig1, dig2, c);
+    });
+  return launch("k_collide_mc", st, [&] {
+    k_collide_mc<32><<<(unsigned)grid, 256, 0, st>>>(seed0, nsched, s1, len1, s2, len2, dig1, dig2, c);
+  });
+}
 
 void pmp_prof_enable(int on) { g_prof.store(on ? 1 : 0); }
 

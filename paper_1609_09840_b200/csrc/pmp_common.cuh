@@ -39,6 +39,54 @@ struct ParamKeys {
   uint64_t r32, b2_32;  // and its two-level r = a_{2,1}, b_2
 };
 
+// ------------------------------------------------------------- key-generation contract
+// (reading Q12; the paper is silent): xoshiro256** seeded with 4 successive
+// splitmix64 outputs of the seed; per level j = 1..8: b_j = x (x >> 32 for
+// 32-bit), then a_{j,1..128} by rejection to [1, p - kappa - 1] (P:543-544,
+// P:619).  Host keygen (pmp_api.cu) and the device Monte Carlo of the quality
+// suite (pmp_misc.cuh) draw from this one implementation.
+struct KeyStream {
+  uint64_t s[4];
+  uint64_t amax;
+  int bits;
+  PMP_HDI static uint64_t splitmix(uint64_t &x) {
+    uint64_t z = (x += 0x9E3779B97F4A7C15ULL);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  }
+  PMP_HDI static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+  PMP_HDI void init(uint64_t seed, int out_bits) {
+    bits = out_bits;
+    amax = out_bits == 64 ? 0xFFFFFFFFFFFFFFF4ULL /* 2^64 - 12 */ : 0xFFFFFFF2ULL /* 2^32 - 14 */;
+    uint64_t x = seed;
+    for (int i = 0; i < 4; i++) s[i] = splitmix(x);
+  }
+  PMP_HDI uint64_t next() {  // xoshiro256**
+    const uint64_t result = rotl(s[1] * 5, 7) * 9;
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return result;
+  }
+  PMP_HDI uint64_t draw_b() {
+    const uint64_t x = next();
+    return bits == 64 ? x : (x >> 32);
+  }
+  PMP_HDI uint64_t draw_a() {
+    uint64_t x;
+    do {
+      x = next();
+      if (bits == 32) x >>= 32;
+    } while (x == 0 || x > amax);
+    return x;
+  }
+};
+
 // ------------------------------------------------------------- helpers
 PMP_DI uint4 ld_stream16(const void *p) {
   uint4 r;

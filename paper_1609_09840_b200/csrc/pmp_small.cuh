@@ -131,3 +131,53 @@ k_small(const ParamKeys K, const uint64_t *__restrict__ blob, const uint64_t *__
 }
 
 }  // namespace pmp
+
+namespace pmp {
+
+// ============================================================= quality suite: collision Monte Carlo
+// SURVEY 8(f2) / SPEC quality_suite collision_monte_carlo (Table 3's almost
+// Delta-universality; "h mod M" stays almost universal):
+// thread i draws the key schedule of seed0 + i on the device (the keygen
+// contract, KeyStream: b_1 then a_{1,0..31}, the only keys a string of <= 127
+// bytes touches) and hashes the fixed pair (s1, s2) with the same short-string
+// path as the batch kernels; counts schedules whose digests are equal in all n
+// bits, and in their low 16 / 12 / 8 bits (the bucket of a table of 2^k).
+template <int BITS>
+__global__ void __launch_bounds__(256)
+k_collide_mc(uint64_t seed0, uint64_t nsched, const uint8_t *__restrict__ s1, uint32_t len1,
+             const uint8_t *__restrict__ s2, uint32_t len2, uint64_t *__restrict__ dig1,
+             uint64_t *__restrict__ dig2, unsigned long long *__restrict__ counts) {
+  __shared__ unsigned long long bc[4];
+  if (threadIdx.x < 4) bc[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nsched) {
+    KeyStream g;
+    g.init(seed0 + i, BITS);
+    ParamKeys K;
+    K.b = g.draw_b();
+#pragma unroll
+    for (int t = 0; t < 32; t++) K.a[t] = g.draw_a();
+    auto one = [&](const uint8_t *sp, uint32_t B) -> uint64_t {
+      const uintptr_t sa = (uintptr_t)sp, se = sa + B, pa = sa & ~(uintptr_t)3;
+      auto fetch = [&](int kk) {
+        const uintptr_t a = pa + 4 * (uintptr_t)kk;
+        return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
+      };
+      const uint64_t lo = short_tree_lo<BITS, false>(K, K.a, B, 8 * (uint32_t)(sa & 3), (int)(B / (BITS / 8)), fetch);
+      return BITS == 64 ? mix64(lo) : (uint64_t)mix32((uint32_t)lo);
+    };
+    const uint64_t d1 = one(s1, len1), d2 = one(s2, len2);
+    if (dig1) dig1[i] = d1;
+    if (dig2) dig2[i] = d2;
+    const uint64_t x = d1 ^ d2;
+    if (x == 0) atomicAdd(&bc[0], 1ull);
+    if ((x & 0xFFFF) == 0) atomicAdd(&bc[1], 1ull);
+    if ((x & 0xFFF) == 0) atomicAdd(&bc[2], 1ull);
+    if ((x & 0xFF) == 0) atomicAdd(&bc[3], 1ull);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && bc[threadIdx.x]) atomicAdd(&counts[threadIdx.x], bc[threadIdx.x]);
+}
+
+}  // namespace pmp

@@ -2,10 +2,11 @@
 
 Inputs are generated on the device (datagen, the shared input generator); the
 oracle regenerates the bytes it needs on the host from the same seeded streams
-(never from the CUDA path's buffers) and recomputes sampled digests one by one.
-configs[3] (one 16 GiB string) is checked in full against the oracle and for
-partition invariance; configs[4] (2^22 strings, ~295 GiB, sized for 8 GPUs) is
-checked on rank 0's byte-balanced shard of 8.
+(never from the CUDA path's buffers).  EVERY digest is compared: configs[1]
+(2^24 strings, both widths), configs[2] (2^20 x 4 KiB), configs[3] (one 16 GiB
+string, plus partition invariance and streaming) and configs[4] (all 2^22
+strings, ~295 GiB, hashed as bench.py's 8 byte-balanced shards one after
+another on this GPU).
 """
 import os
 from concurrent.futures import ThreadPoolExecutor
@@ -67,29 +68,34 @@ def _check_sample(oracle_lib, keys_o, seed, offs, got, idx, base_byte=0):
     assert not bad, bad[:10]
 
 
-@pytest.mark.parametrize("bits", [64, 32])
-def test_hashtable_full_size_sampled(dev, oracle_lib, bits):
-    """configs[1]: 2^24 strings U[8,64] B, seed 2 -- all hashed on the GPU,
-    20,000 random + first/last 500 digests recomputed by the oracle."""
-    import torch
+def _oracle_all(oracle_lib, keys_o, seed, offs, base_byte=0, piece=2 << 30):
+    """Every digest of the batch with CSR ``offs`` (relative to payload byte
+    ``base_byte`` of the seeded stream) by the multithreaded oracle, the payload
+    regenerated on the host piece by piece (string-aligned pieces of ~2 GiB)."""
+    n = offs.size - 1
+    out = np.empty(n, dtype=np.uint64)
+    i = 0
+    while i < n:
+        j = int(np.searchsorted(offs, np.uint64(int(offs[i]) + piece), side="right")) - 1
+        j = min(max(j, i + 1), n)
+        o0 = int(offs[i])
+        pay = host_payload_parallel(seed, base_byte + o0, int(offs[j]) - o0)
+        out[i:j] = oracle_lib.hash_batch(keys_o, pay, offs[i:j + 1] - np.uint64(o0), nthreads=NT)
+        i = j
+    return out
 
-    wl = datagen.WORKLOADS["hashtable"]
-    offs = datagen.offsets_from_lengths(wl.lengths())
-    pay, d_off = _device_batch(dev, wl.seed, offs)
-    keys = pmp.Keys.generate(wl.seed, bits)
-    got = pmp.as_u64(pmp.hash_batch(keys, pay, d_off))
-    torch.cuda.synchronize()
-    n = wl.n
-    rng = np.random.default_rng(bits)
-    idx = np.unique(np.concatenate([rng.integers(0, n, 20000), np.arange(500), np.arange(n - 500, n)]))
-    _check_sample(oracle_lib, oracle_lib.keygen(wl.seed, bits), wl.seed, offs, got, idx)
+
+def _assert_all_equal(got, want, bits):
+    want = want.astype(np.uint64) if bits == 64 else want.astype(np.uint32)
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (bad.size, bad[:10])
 
 
-def test_hashtable_full_size_fused_both_widths(dev, oracle_lib):
-    """configs[1] in bench.py's launch configuration: both widths in one fused
-    pass (pmp_hash_batch_multi); 20,000 random + first/last 500 digests of
-    each width recomputed by the oracle, and both equal the per-width launches
-    on a further 100,000 indices."""
+def test_hashtable_full_size_every_hash(dev, oracle_lib):
+    """configs[1] in bench.py's launch configuration: 2^24 strings U[8,64] B,
+    seed 2, both widths in one fused pass (pmp_hash_batch_multi).  EVERY digest
+    of both widths equals the oracle's, and so do the per-width launches
+    (pmp_hash_batch, the k_short single-width kernels)."""
     import torch
 
     wl = datagen.WORKLOADS["hashtable"]
@@ -101,17 +107,18 @@ def test_hashtable_full_size_fused_both_widths(dev, oracle_lib):
     s32 = pmp.hash_batch(k32, pay, d_off)
     torch.cuda.synchronize()
     g64, g32 = pmp.as_u64(o64), pmp.as_u64(o32)
-    n = wl.n
-    rng = np.random.default_rng(64 + 32)
-    idx = np.unique(np.concatenate([rng.integers(0, n, 20000), np.arange(500), np.arange(n - 500, n)]))
-    _check_sample(oracle_lib, oracle_lib.keygen(wl.seed, 64), wl.seed, offs, g64, idx)
-    _check_sample(oracle_lib, oracle_lib.keygen(wl.seed, 32), wl.seed, offs, g32, idx)
-    j = rng.integers(0, n, 100000)
-    assert np.array_equal(g64[j], pmp.as_u64(s64)[j]) and np.array_equal(g32[j], pmp.as_u64(s32)[j])
+    del pay
+    torch.cuda.empty_cache()
+    w64 = _oracle_all(oracle_lib, oracle_lib.keygen(wl.seed, 64), wl.seed, offs)
+    _assert_all_equal(g64, w64, 64)
+    _assert_all_equal(pmp.as_u64(s64), w64, 64)
+    w32 = _oracle_all(oracle_lib, oracle_lib.keygen(wl.seed, 32), wl.seed, offs)
+    _assert_all_equal(g32, w32, 32)
+    _assert_all_equal(pmp.as_u64(s32), w32, 32)
 
 
-def test_fixed4k_full_size_sampled(dev, oracle_lib):
-    """configs[2]: 2^20 x 4096 B (4 GiB), PM+64, seed 3; 3,000 sampled digests."""
+def test_fixed4k_full_size_every_hash(dev, oracle_lib):
+    """configs[2]: 2^20 x 4096 B (4 GiB), PM+64, seed 3 -- every digest."""
     import torch
 
     wl = datagen.WORKLOADS["fixed4k"]
@@ -120,11 +127,9 @@ def test_fixed4k_full_size_sampled(dev, oracle_lib):
     keys = pmp.Keys.generate(wl.seed, 64)
     got = pmp.as_u64(pmp.hash_batch(keys, pay, d_off))
     torch.cuda.synchronize()
-    rng = np.random.default_rng(3)
-    idx = np.unique(np.concatenate([rng.integers(0, wl.n, 3000), [0, wl.n - 1]]))
-    _check_sample(oracle_lib, oracle_lib.keygen(wl.seed, 64), wl.seed, offs, got, idx)
     del pay
     torch.cuda.empty_cache()
+    _assert_all_equal(got, _oracle_all(oracle_lib, oracle_lib.keygen(wl.seed, 64), wl.seed, offs), 64)
 
 
 def test_long16g_full(dev, oracle_lib):
@@ -168,24 +173,25 @@ def test_long16g_full(dev, oracle_lib):
     assert got2 == oracle_lib.hash2(okeys, host, nthreads=NT)
 
 
-def test_mixed_shard_sampled(dev, oracle_lib):
+def test_mixed_corpus_every_hash(dev, oracle_lib):
     """configs[4]: 2^22 strings, log-uniform [1, 2^20] B, PM+32, seed 5 (~295 GiB
-    in total, reading Q15).  Rank 0's byte-balanced shard of 8 (~37 GiB) is hashed
-    on the GPU; 3,000 random strings and the 40 longest are checked."""
+    in total, reading Q15).  The 8 byte-balanced shards of bench.py's 8-GPU
+    split are hashed one after another on this GPU (pmp_hash_batch, rebased
+    offsets, as each rank does) and EVERY digest of the corpus equals the
+    oracle's (payload regenerated on the host piece by piece)."""
     import torch
 
     wl = datagen.WORKLOADS["mixed"]
     offs_all = datagen.offsets_from_lengths(wl.lengths())
-    lo, hi = parallel.shard_batch(offs_all, 8)[0]
-    sub, b0, b1 = parallel.rebase_offsets(offs_all, lo, hi)
-    pay, d_off = _device_batch(dev, wl.seed, offs_all[lo:hi + 1], start_byte=b0)
     keys = pmp.Keys.generate(wl.seed, 32)
-    got = pmp.as_u64(pmp.hash_batch(keys, pay, d_off))
-    torch.cuda.synchronize()
-    n = hi - lo
-    lens = np.diff(sub.astype(np.int64))
-    rng = np.random.default_rng(5)
-    idx = np.unique(np.concatenate([rng.integers(0, n, 3000), np.argsort(lens)[-40:], [0, n - 1]]))
-    _check_sample(oracle_lib, oracle_lib.keygen(wl.seed, 32), wl.seed, sub, got, idx, base_byte=b0)
-    del pay
-    torch.cuda.empty_cache()
+    okeys = oracle_lib.keygen(wl.seed, 32)
+    shards = parallel.shard_batch(offs_all, 8)
+    assert shards[0][0] == 0 and shards[-1][1] == wl.n
+    for lo, hi in shards:
+        sub, b0, b1 = parallel.rebase_offsets(offs_all, lo, hi)
+        pay, d_off = _device_batch(dev, wl.seed, offs_all[lo:hi + 1], start_byte=b0)
+        got = pmp.as_u64(pmp.hash_batch(keys, pay, d_off))
+        torch.cuda.synchronize()
+        del pay, d_off
+        torch.cuda.empty_cache()
+        _assert_all_equal(got, _oracle_all(oracle_lib, okeys, wl.seed, sub, base_byte=b0), 32)

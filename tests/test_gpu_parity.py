@@ -412,16 +412,57 @@ def test_bucket_partition(torch_dev, oracle_lib, M, n):
 
 # ------------------------------------------------------------ quality suite
 @pytest.mark.parametrize("bits,length", [(64, 8), (64, 16), (32, 4), (32, 12)])
-def test_avalanche_bias_small(torch_dev, bits, length):
+def test_avalanche_bias_small(torch_dev, oracle_lib, bits, length):
     """SPEC S:437 threshold (worst bias < 0.03); 3e4 trials keep the binomial
     noise (sd 0.003) far below it.  The digest path is cross-checked against
     the oracle on one trial's batch."""
     from paper_1609_09840_b200 import quality
 
     keys = pmp.Keys.generate(77, bits)
-    worst, freq = quality.avalanche(keys, length, 30000, seed=5)
+    worst, freq, (pay, off, dig) = quality.avalanche(keys, length, 30000, seed=5, first_batch=True)
     assert freq.shape == (8 * length, bits)
     assert worst < 0.03, worst
+    # the digests the statistics came from: the first chunk's batch (4096 inputs
+    # and all their single-bit flips) recomputed by the oracle, digest by digest
+    want = oracle_batch(oracle_lib, 77, bits, pay, off)
+    assert np.array_equal(dig, want)
+
+
+@pytest.mark.parametrize("bits", [32, 64])
+def test_collision_monte_carlo(torch_dev, oracle_lib, bits):
+    """SPEC quality_suite collision_monte_carlo (Table 3 P:644-646,
+    h mod M P:188-192): for fixed pairs, 10^6 device-drawn key schedules.
+    The first 1,000 schedules' digests of both strings equal the oracle's with
+    keygen(seed0 + i); distinct pairs never collide in all n bits (rate <= 1e-4,
+    expected 0); low-8 / low-16-bit collisions (buckets of 2^8 / 2^16-entry
+    tables) occur at rate 2^-k within 6 sigma; the (s, s) control collides
+    always; sub-word strings (|sigma| = 1, reading Q2) are key-independent."""
+    from paper_1609_09840_b200 import quality
+
+    rng = np.random.default_rng(bits)
+    a = bytes(rng.integers(0, 256, 37, dtype=np.uint8))
+    b = bytearray(a)
+    b[5] ^= 0x10                                   # one bit apart
+    pairs = [(a, bytes(b)), (a[:12], a[1:13]), (a[:1], a[:2] if bits == 64 else a[:3]), (b"", b"\x00"),
+             (a + a[:90], a[::-1] + a[:90])]
+    N = 1_000_000
+    seed0 = 1 << 33
+    for s1, s2 in pairs:
+        r = quality.collision_monte_carlo(bits, s1, s2, 1000, seed0=seed0, return_digests=True)
+        g1, g2 = r["digests"]
+        ok1 = [oracle_lib.hash_bytes(oracle_lib.keygen(seed0 + i, bits), s1) for i in range(0, 1000, 7)]
+        ok2 = [oracle_lib.hash_bytes(oracle_lib.keygen(seed0 + i, bits), s2) for i in range(0, 1000, 7)]
+        assert [int(x) for x in g1[::7]] == ok1 and [int(x) for x in g2[::7]] == ok2, (s1, s2)
+        r = quality.collision_monte_carlo(bits, s1, s2, N, seed0=seed0)
+        assert r["full"] == 0 and r["rate_full"] <= 1e-4, (s1, s2, r)
+        if len(s1) >= bits // 8 or len(s2) >= bits // 8:
+            for k, key in ((8, "rate_low8"), (16, "rate_low16")):
+                pk = 2.0 ** -k
+                assert abs(r[key] - pk) <= 6 * (pk * (1 - pk) / N) ** 0.5 + 1e-9, (k, r)
+        else:                                      # both |sigma| = 1: digests do not depend on the keys
+            assert r["low8"] in (0, N) and r["low16"] in (0, N)
+    r = quality.collision_monte_carlo(bits, a, a, N, seed0=seed0)
+    assert r["full"] == r["low16"] == r["low8"] == N
 
 
 @pytest.mark.parametrize("bits", [32, 64])
