@@ -656,6 +656,23 @@ void pmp_keys_free(pmp_keys *k) {
   delete k;
 }
 
+// A launch with programmatic dependent launch (PDL): the grid may be scheduled
+// before the previous kernel on the stream completes; it must start with
+// griddepcontrol.wait before touching that kernel's results (k_wstring).
+static void launch_pdl(const void *f, unsigned grid, unsigned threads, void **args, size_t smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelExC(&cfg, f, args);
+}
+
 // Resident blocks per SM of a kernel (registers, shared memory), cached: the
 // persistent grids are exactly one wave.
 static int resident_blocks(const void *f, int threads, size_t smem, const char *name) {
@@ -764,7 +781,7 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     return launch("k_wstring", st, [&] {
       void *args[] = {(void *)&blob, (void *)&bytes, (void *)&offsets, (void *)&n, (void *)&o, (void *)&wlist,
                       (void *)&wcount};
-      cudaLaunchKernel(kw, dim3(wgrid), dim3(kWBlockWarps * 32), args, kWSmem, st);
+      launch_pdl(kw, wgrid, kWBlockWarps * 32, args, kWSmem, st);
     });
   };
   if (!dual) return launch_w(k, os);
@@ -776,7 +793,7 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   return launch("k_wstring", st, [&] {
     void *args[] = {(void *)&b64, (void *)&b32, (void *)&bytes, (void *)&offsets, (void *)&n, (void *)&os,
                     (void *)&o32, (void *)&wlist, (void *)&wcount};
-    cudaLaunchKernel(kw, dim3(wgrid), dim3(kWBlockWarps * 32), args, kWSmem, st);
+    launch_pdl(kw, wgrid, kWBlockWarps * 32, args, kWSmem, st);
   });
 }
 

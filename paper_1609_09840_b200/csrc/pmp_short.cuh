@@ -110,7 +110,11 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   // exit test granularity: the warp maximum is 7 or 8 full words for configs[1],
   // so the tree pass tests once per 8 words (measured +0.9%; the two-level pass
   // and the single-width kernels are faster with 4)
+#if PMP_SHORT_DIAG >= 3
+  constexpr int G = 4;
+#else
   constexpr int G = V2 ? kShortG64 : 8;
+#endif
 #pragma unroll
   for (int tb = 0; tb < 16; tb += G) {
     if (tb >= tfull_max) break;                              // warp-uniform
@@ -127,9 +131,13 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
       const bool f64 = t < tl64;
       const uint32_t lm = f64 ? lo : 0u, hm = f64 ? hi : 0u;
       if (t < 15) {
+#if PMP_SHORT_DIAG != 7   // (diagnostic builds 6 / 7: one width's loop multiply-adds left out)
         mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lm, hm);  // Eq. (1)
+#endif
+#if PMP_SHORT_DIAG != 6
         mac32(C, K.a32[2 * t], lm);
         mac32(C, K.a32[2 * t + 1], hm);
+#endif
       }
     }
   }
@@ -189,8 +197,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
 // tile whose span exceeds kSpanMaxTile is "direct": consumers read its short
 // strings from global.  Strings longer than kShortMax are appended by the
 // consumers to the work list of k_wstring in either mode.
-constexpr int kPasses = 1;                                     // strings per consumer lane per tile
-constexpr int kTile = 32 * kShortWarps * kPasses;              // 384
+constexpr int kTile = 32 * kShortWarps;                        // 512 strings per tile (16 consumer warps)
 #ifndef PMP_SHORT_SLOTS
 #define PMP_SHORT_SLOTS 8
 #endif
@@ -218,12 +225,27 @@ constexpr size_t kShortSmem = 384 /* keys */ + kByteRing + kSlack + 16 + (size_t
                               (size_t)(3 * kRing) * 8 + 128;
 
 // DUAL: BITS = 64 and a second, 32-bit schedule in K.a32 / K.b32 whose digests go to os2
+// (tuning builds: PMP_SHORT_MINB = min resident blocks for ptxas, PMP_SHORT_MAXNREG
+// = register cap; the product build sets neither: ptxas then lands at 56
+// registers, two 17-warp blocks per SM -- an explicit minBlocks of 1 gives 64
+// registers and ONE block per SM, 13% slower)
 template <int BITS, bool V2 = false, bool DUAL = false>
+#if defined(PMP_SHORT_MAXNREG)
+__global__ void __maxnreg__(PMP_SHORT_MAXNREG)
+#elif defined(PMP_SHORT_MINB)
+__global__ void __launch_bounds__((kShortWarps + 1) * 32, PMP_SHORT_MINB)
+#else
 __global__ void __launch_bounds__((kShortWarps + 1) * 32)
+#endif
 k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets,
         uint64_t n, const OutSpec os, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount,
         const OutSpec os2) {
   extern __shared__ __align__(128) uint8_t smem[];
+  // let the dependent k_wstring grid (programmatic dependent launch) be
+  // scheduled now: its blocks take SM slots as this grid's blocks retire and
+  // wait in griddepcontrol.wait for this grid's completion, so the launch
+  // latency of the long-string pass overlaps this grid's tail
+  asm volatile("griddepcontrol.launch_dependents;");
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint64_t *skeys = reinterpret_cast<uint64_t *>(smem);                       // a_{1,0..31}
   uint32_t *skeys32 = reinterpret_cast<uint32_t *>(smem + 256);               // DUAL: 32-bit a_{1,0..31}
@@ -346,8 +368,12 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         hdr[q].alo = (uint64_t)alo;
         hdr[q].pos = pos;
         hdr[q].mode = mode | (tid << 2);     // the consumers' tile index
+#if PMP_SHORT_DIAG == 2 || PMP_SHORT_DIAG == 4  // diagnostic build: hashing only (the byte copies skipped, ring bytes stale)
+        mbar_arrive_tx(&bar_full[q], 0);
+#else
         mbar_arrive_tx(&bar_full[q], nb);   // release: hdr and offsets visible to consumers
         if (nb) bulk_g2s(ring + pos, reinterpret_cast<const void *>(alo), nb, &bar_full[q]);
+#endif
       }
       __syncwarp();
       // claim + offsets of tile k + kOffAhead after tile k's bytes are on their
@@ -396,7 +422,11 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
       if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
     }
     // warp max of the number of full words (the marker word is handled apart)
+#if PMP_SHORT_DIAG >= 3  // diagnostic build: the word loop capped at 4 words (what padding costs); 5: no loop
+    const int tfm = min(PMP_SHORT_DIAG == 5 ? 0 : 4, (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u));
+#else
     const int tfm = (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
+#endif
     if (is_short) {
       uint64_t lo;
       uint32_t lo32 = 0;
@@ -405,7 +435,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         const uint32_t sofs = rpos + (valid ? (uint32_t)((uintptr_t)(bytes + o0) - (uintptr_t)ralo) : 0u);
         const uint32_t pa = ring_s + (sofs & ~3u);
         auto fetch = [&](int kk) { return lds_u32(pa + 4 * kk); };
-#if PMP_SHORT_DIAG  // diagnostic build: the data pipeline alone (one shared load per string, no hashing)
+#if PMP_SHORT_DIAG == 1  // diagnostic build: the data pipeline alone (one shared load per string, no hashing)
         lo = fetch(0) ^ B;
         lo32 = (uint32_t)lo;
         if (0)

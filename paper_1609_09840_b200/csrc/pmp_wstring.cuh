@@ -456,6 +456,9 @@ __device__ __forceinline__ void wstring_body(const uint64_t *__restrict__ keys, 
   WStack *stk = reinterpret_cast<WStack *>(bar + kWStages);
   const uint64_t *bk = keys;           // b_1..b_8
   const uint64_t *ak = keys + kL;      // a_{j,i} at ak[(j-1)*128 + i]
+  // launched with programmatic dependent launch after k_short (pmp_api.cu): the
+  // work list is k_short's output, so wait for that grid (and its memory) first
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t nmid = wcount[0], nbig = wcount[1];
   if (nmid + nbig == 0) return;
   for (int k = threadIdx.x; k < (int)kM; k += blockDim.x) {

@@ -64,6 +64,56 @@ __global__ void k_shf(uint32_t *out, uint32_t a, uint32_t b) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void k_dfma(double *out, uint32_t a, uint32_t b) {
+  double x[8];
+  const double m = 1.0 + 1e-9 * a, c = 1e-7 * b;
+  for (int j = 0; j < 8; j++) x[j] = threadIdx.x + j;
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[j]) : "d"(m), "d"(c));
+  }
+  double s = 0;
+  for (int j = 0; j < 8; j++) s += x[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// one IMAD.WIDE.U32 and one DFMA per chain step: do the fma-heavy and the
+// fp64 pipes overlap (sum of the two rates) or share a limit?
+__global__ void k_wide_plus_dfma(double *out, uint32_t a, uint32_t b) {
+  uint64_t acc[8];
+  double x[8];
+  const double m = 1.0 + 1e-9 * a, c = 1e-7 * b;
+  for (int j = 0; j < 8; j++) { acc[j] = threadIdx.x + j; x[j] = j; }
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc[j]) : "r"(a + j), "r"(b + (uint32_t)it));
+      asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[j]) : "d"(m), "d"(c));
+    }
+  }
+  double s = 0;
+  for (int j = 0; j < 8; j++) s += x[j] + (double)acc[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// u32 -> f64 via the magic-exponent trick: (2^52 | s) as bits, minus 2^52 (exact)
+__global__ void k_u2d_magic(double *out, uint32_t a, uint32_t b) {
+  double x[8];
+  for (int j = 0; j < 8; j++) x[j] = j;
+  uint32_t v = threadIdx.x;
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const double d = __hiloint2double(0x43300000, (int)(v + j * b)) - 4503599627370496.0;
+      asm volatile("fma.rn.f64 %0, %1, %2, %0;" : "+d"(x[j]) : "d"(d), "d"((double)a));
+    }
+    v += a;
+  }
+  double s = 0;
+  for (int j = 0; j < 8; j++) s += x[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <class K, class T>
 double run(K kern, T *buf, int blocks, int threads, int sass_per_op) {
   cudaEvent_t e0, e1;
@@ -93,6 +143,9 @@ int main() {
          run(k_mad_wide_cc, (uint32_t *)buf, blocks, threads, 1));
   printf(" \"IMAD.WIDE.U32 (64-bit accumulate, no carry)\": %.3f,\n", run(k_mad_wide, (uint64_t *)buf, blocks, threads, 1));
   printf(" \"IADD3\": %.3f,\n", run(k_iadd3, (uint32_t *)buf, blocks, threads, 1));
-  printf(" \"SHF.R.W (funnel shift)\": %.3f}\n", run(k_shf, (uint32_t *)buf, blocks, threads, 1));
+  printf(" \"SHF.R.W (funnel shift)\": %.3f,\n", run(k_shf, (uint32_t *)buf, blocks, threads, 1));
+  printf(" \"DFMA\": %.3f,\n", run(k_dfma, (double *)buf, blocks, threads, 1));
+  printf(" \"IMAD.WIDE + DFMA pairs (pairs per cycle)\": %.3f,\n", run(k_wide_plus_dfma, (double *)buf, blocks, threads, 1));
+  printf(" \"u32->f64 magic (MOV/DADD) + DFMA (per value)\": %.3f}\n", run(k_u2d_magic, (double *)buf, blocks, threads, 1));
   return 0;
 }
