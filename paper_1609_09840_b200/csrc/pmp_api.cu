@@ -760,7 +760,7 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   const void *kshort = dual ? (v2 ? (const void *)k_short<64, true, true> : (const void *)k_short<64, false, true>)
                             : v2 ? (k->bits == 64 ? (const void *)k_short<64, true> : (const void *)k_short<32, true>)
                                  : (k->bits == 64 ? (const void *)k_short<64> : (const void *)k_short<32>);
-  const int threads = (kShortWarps + 1) * 32;  // + producer warp
+  const int threads = kShortThreads;  // consumers + producer (+ sorter) warps
   uint64_t grid = (n + kTile - 1) / kTile;
   const uint64_t maxgrid = (uint64_t)sms * resident_blocks(kshort, threads, kShortSmem, "k_short");  // persistent grid
   if (grid > maxgrid) grid = maxgrid;

@@ -207,7 +207,8 @@ constexpr int kTile = 32 * kShortWarps;                        // 512 strings pe
 constexpr int kRing = PMP_SHORT_SLOTS, kOffAhead = PMP_SHORT_OFF_AHEAD;  // tile slots (power of 2), offsets prefetch
 constexpr uint32_t kByteRing = PMP_SHORT_RING_KB * 1024;
 // (Length sorting / partitioning of the tiles, to cut the zero-padding
-// multiply-adds, was measured five ways and never paid: profiles/r01f.)
+// multiply-adds, was measured five ways in round 1 and with a dedicated sorter
+// warp in round 2 -- 2x slower: profiles/r01f, profiles/r02/README.md.)
 constexpr uint32_t kSpanMaxTile = kByteRing / 2 < 32 * 1024 ? kByteRing / 2 : 32 * 1024;  // larger spans go direct
 constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
 constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
@@ -220,6 +221,7 @@ struct TileHdr {
   uint32_t pos;    // ring position of staged byte 0
   uint32_t mode;   // bits 0-1: 0 staged, 1 direct; bits 2-31: tile index; kModeEnd: no more tiles
 };
+constexpr int kShortThreads = (kShortWarps + 1) * 32;     // consumer warps + the producer warp
 constexpr size_t kShortSmem = 384 /* keys */ + kByteRing + kSlack + 16 + (size_t)kRing * kOffBytes +
                               (size_t)kRing * sizeof(TileHdr) +
                               (size_t)(3 * kRing) * 8 + 128;
@@ -233,9 +235,9 @@ template <int BITS, bool V2 = false, bool DUAL = false>
 #if defined(PMP_SHORT_MAXNREG)
 __global__ void __maxnreg__(PMP_SHORT_MAXNREG)
 #elif defined(PMP_SHORT_MINB)
-__global__ void __launch_bounds__((kShortWarps + 1) * 32, PMP_SHORT_MINB)
+__global__ void __launch_bounds__(kShortThreads, PMP_SHORT_MINB)
 #else
-__global__ void __launch_bounds__((kShortWarps + 1) * 32)
+__global__ void __launch_bounds__(kShortThreads)
 #endif
 k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets,
         uint64_t n, const OutSpec os, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount,
