@@ -1191,6 +1191,15 @@ uint64_t pmp_launch_count(void) { return g_launches.load(); }
 
 uint64_t pmp_set_small_batch_max(uint64_t n) { return g_small_max.exchange(n); }
 
+#if PMP_SHORT_TRACE
+// diagnostic builds only: the k_short clock64 timeline (pmp_short.cuh)
+int pmp_trace_read(uint64_t *out, uint64_t n) {
+  const uint64_t cap = sizeof(g_trace) / 8;
+  if (n > cap) n = cap;
+  return cudaMemcpyFromSymbol(out, g_trace, n * 8) == cudaSuccess ? (int)n : PMP_ECUDA;
+}
+#endif
+
 int pmp_quality_collisions(int out_bits, uint64_t seed0, uint64_t nsched, const uint8_t *s1, uint32_t len1,
                            const uint8_t *s2, uint32_t len2, uint64_t *dig1, uint64_t *dig2, uint64_t *counts,
                            cudaStream_t st) {

@@ -226,6 +226,23 @@ constexpr size_t kShortSmem = 384 /* keys */ + kByteRing + kSlack + 16 + (size_t
                               (size_t)kRing * sizeof(TileHdr) +
                               (size_t)(3 * kRing) * 8 + 128;
 
+#ifndef PMP_SHORT_TRACE
+#define PMP_SHORT_TRACE 0
+#endif
+#if PMP_SHORT_TRACE  // diagnostic build: clock64 timeline of blocks 0 and 1 (pmp_trace_read)
+constexpr int kTrTiles = 256;
+__device__ unsigned long long g_trace[2][kShortWarps + 1][kTrTiles][4];
+#define PMP_TR(w, k, e)                                                                   \
+  do {                                                                                    \
+    if (blockIdx.x < 2 && lane == 0 && (k) < (uint32_t)kTrTiles)                          \
+      g_trace[blockIdx.x][(w)][(k)][(e)] = clock64();                                     \
+  } while (0)
+#else
+#define PMP_TR(w, k, e) \
+  do {                  \
+  } while (0)
+#endif
+
 // DUAL: BITS = 64 and a second, 32-bit schedule in K.a32 / K.b32 whose digests go to os2
 // (tuning builds: PMP_SHORT_MINB = min resident blocks for ptxas, PMP_SHORT_MAXNREG
 // = register cap; the product build sets neither: ptxas then lands at 56
@@ -330,8 +347,10 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         }
         break;
       }
+      PMP_TR(kShortWarps, k, 3);
       mbar_wait(&bar_off[q], (k / kRing) & 1);
       __syncwarp();
+      PMP_TR(kShortWarps, k, 0);
       const uint32_t tid = tids[q];
       const uint64_t base = (uint64_t)tid * kTile;
       const uint32_t nv = (uint32_t)min((uint64_t)kTile, n - base);  // strings in this tile
@@ -365,6 +384,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         oldest++;
       }
       __syncwarp();
+      PMP_TR(kShortWarps, k, 1);
       if (lane == 0) {
         tend[q] = head;
         hdr[q].alo = (uint64_t)alo;
@@ -378,6 +398,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
 #endif
       }
       __syncwarp();
+      PMP_TR(kShortWarps, k, 2);
       // claim + offsets of tile k + kOffAhead after tile k's bytes are on their
       // way (the claim is a global atomic round trip)
       if (k_end == 0xffffffffu) issue_offs(k + kOffAhead);
@@ -392,7 +413,9 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   const uint32_t ct = 32u * wib + lane;                 // consumer thread = string slot in the tile
   for (uint32_t k = 0;; k++) {
     const uint32_t q = k & (kRing - 1);
+    PMP_TR(wib, k, 0);
     mbar_wait_s(full_s + 8 * q, (k / kRing) & 1);
+    PMP_TR(wib, k, 1);
     uint64_t ralo;
     uint32_t rpos, mode;
     lds_hdr(hdr_s + 16 * q, ralo, rpos, mode);
@@ -462,6 +485,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
       }
     }
     __syncwarp();
+    PMP_TR(wib, k, 2);
     if (lane == 0) mbar_arrive_s(done_s + 8 * q);
   }
 }
