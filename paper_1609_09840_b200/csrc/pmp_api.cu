@@ -947,6 +947,27 @@ int pmp_hash_batch_host(const pmp_keys *const *keys, int nkeys, const uint8_t *b
     }
   } guard{cur_dev, dev};
   if (cur_dev != dev && cudaSetDevice(dev) != cudaSuccess) return PMP_ECUDA;
+  if (cut.size() == 2) {
+    // one piece (a small batch): nothing to overlap, so no internal streams or
+    // events -- H2D, hash, D2H in order on the caller's stream, one scratch slab
+    const uint64_t b0 = offsets[0], nb = offsets[n] - b0, sh = b0 & 15;
+    const size_t cap_b = ((size_t)nb + 48 + 255) & ~(size_t)255, cap_o = ((size_t)(n + 1) * 8 + 255) & ~(size_t)255;
+    const size_t cap_d = ((size_t)n * 8 + 255) & ~(size_t)255;
+    uint8_t *slab = nullptr;
+    if (cudaMallocAsync((void **)&slab, cap_b + cap_o + (size_t)nkeys * cap_d, stream) != cudaSuccess) return PMP_ENOMEM;
+    uint64_t *d_o = (uint64_t *)(slab + cap_b);
+    void *d_outs[PMP_HOST_MAX_KEYS];
+    for (int k = 0; k < nkeys; k++) d_outs[k] = slab + cap_b + cap_o + (size_t)k * cap_d;
+    int rc = 0;
+    if (nb && cudaMemcpyAsync(slab + sh, bytes + b0, nb, cudaMemcpyHostToDevice, stream) != cudaSuccess) rc = PMP_ECUDA;
+    if (!rc && cudaMemcpyAsync(d_o, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, stream) != cudaSuccess) rc = PMP_ECUDA;
+    if (!rc) rc = pmp_hash_batch_multi(keys, nkeys, slab + sh - b0, d_o, n, d_outs, stream);
+    for (int k = 0; k < nkeys && !rc; k++)
+      if (cudaMemcpyAsync(outs[k], d_outs[k], n * (keys[k]->bits / 8), cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+        rc = PMP_ECUDA;
+    cudaFreeAsync(slab, stream);
+    return rc;
+  }
   {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_host_st[dev].init) {
@@ -1197,6 +1218,11 @@ int pmp_trace_read(uint64_t *out, uint64_t n) {
   const uint64_t cap = sizeof(g_trace) / 8;
   if (n > cap) n = cap;
   return cudaMemcpyFromSymbol(out, g_trace, n * 8) == cudaSuccess ? (int)n : PMP_ECUDA;
+}
+int pmp_trace_blocks(uint64_t *out, uint64_t n) {
+  const uint64_t cap = sizeof(g_trace_blk) / 8;
+  if (n > cap) n = cap;
+  return cudaMemcpyFromSymbol(out, g_trace_blk, n * 8) == cudaSuccess ? (int)n : PMP_ECUDA;
 }
 #endif
 

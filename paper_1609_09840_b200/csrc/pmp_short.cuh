@@ -232,6 +232,7 @@ constexpr size_t kShortSmem = 384 /* keys */ + kByteRing + kSlack + 16 + (size_t
 #if PMP_SHORT_TRACE  // diagnostic build: clock64 timeline of blocks 0 and 1 (pmp_trace_read)
 constexpr int kTrTiles = 256;
 __device__ unsigned long long g_trace[2][kShortWarps + 1][kTrTiles][4];
+__device__ unsigned long long g_trace_blk[1024][3];   // per block: smid, tiles consumed, end clock
 #define PMP_TR(w, k, e)                                                                   \
   do {                                                                                    \
     if (blockIdx.x < 2 && lane == 0 && (k) < (uint32_t)kTrTiles)                          \
@@ -419,7 +420,18 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     uint64_t ralo;
     uint32_t rpos, mode;
     lds_hdr(hdr_s + 16 * q, ralo, rpos, mode);
-    if (mode == kModeEnd) break;
+    if (mode == kModeEnd) {
+#if PMP_SHORT_TRACE
+      if (wib == 0 && lane == 0 && blockIdx.x < 1024) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_trace_blk[blockIdx.x][0] = smid;
+        g_trace_blk[blockIdx.x][1] = k;
+        g_trace_blk[blockIdx.x][2] = clock64();
+      }
+#endif
+      break;
+    }
     const uint64_t ibase = (uint64_t)(mode >> 2) * kTile;
     mode &= 3;
     uint64_t i = ibase + ct;

@@ -61,6 +61,21 @@ def main():
                             "wait_fraction": float(waits.sum() / (waits.sum() + hashes.sum())),
                             "hash_cycles_per_warp_min_max": [float(hashes.mean(axis=1).min()), float(hashes.mean(axis=1).max())],
                             "first_tiles": rows}
+    lib.pmp_trace_blocks.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+    lib.pmp_trace_blocks.restype = ctypes.c_int
+    bb = np.zeros(1024 * 3, dtype=np.uint64)
+    lib.pmp_trace_blocks(bb.ctypes.data, bb.size)
+    bb = bb.reshape(1024, 3).astype(np.int64)
+    used = bb[:, 1] > 0
+    per_sm = {}
+    for smid, tiles in bb[used, :2]:
+        per_sm.setdefault(int(smid), []).append(int(tiles))
+    pairs = sorted(per_sm.values())
+    tiles_sm = np.array([sum(v) for v in per_sm.values()])
+    blk = bb[used, 1]
+    out["blocks"] = {"n": int(used.sum()), "tiles_per_block_min_mean_max": [int(blk.min()), float(blk.mean()), int(blk.max())],
+                     "sms": len(per_sm), "tiles_per_sm_min_mean_max": [int(tiles_sm.min()), float(tiles_sm.mean()), int(tiles_sm.max())],
+                     "per_sm_block_tiles_sample": pairs[:5] + pairs[-5:]}
     print(json.dumps({"read": got, **out}, indent=1))
 
 
