@@ -6,7 +6,9 @@
  * Input (stdin, text): bits n, then n lengths, then the payload is generated as
  * byte i = (i * 131 + 7) & 255 over the concatenation.  Output (stdout): one
  * line per string for pmp_hash_batch, the same via pmp_hash_batch_host, then
- * pmp_hash_long of the whole concatenation, and pmp_stream_* of it in 3 pieces.
+ * pmp_hash_long of the whole concatenation, pmp_stream_* of it in 3 pieces,
+ * pmp_hash_long_host of it from host memory, and the batch again through the
+ * throughput path (pmp_set_small_batch_max(0)).
  */
 #include <cuda_runtime.h>
 #include <inttypes.h>
@@ -101,6 +103,20 @@ int main(void) {
   CU(cudaMemcpy(out, d_out, w, cudaMemcpyDeviceToHost));
   printf("stream %016" PRIx64 "\n", digest_at(out, bits, 0));
   pmp_stream_free(s);
+
+  /* the concatenation from pinned HOST memory, streamed in 2 KiB pieces */
+  uint64_t hdig = 0;
+  CK(pmp_hash_long_host(k, bytes, total, &hdig, 2048, st));
+  CU(cudaStreamSynchronize(st));
+  printf("longhost %016" PRIx64 "\n", bits == 64 ? hdig : (uint64_t)(uint32_t)hdig);
+
+  /* the latency path (k_small) and the throughput path give the same digests */
+  const uint64_t prev = pmp_set_small_batch_max(0);
+  CK(pmp_hash_batch(k, d_bytes, d_off, n, d_out, st));
+  CU(cudaStreamSynchronize(st));
+  CU(cudaMemcpy(out, d_out, n * w, cudaMemcpyDeviceToHost));
+  pmp_set_small_batch_max(prev);
+  for (uint64_t i = 0; i < n; i++) printf("tput %" PRIu64 " %016" PRIx64 "\n", i, digest_at(out, bits, i));
 
   /* errors are reported, not crashed on */
   printf("einval %d\n", pmp_hash_batch(k, NULL, d_off, n ? n : 1, d_out, st));

@@ -62,4 +62,6 @@ def test_c_client_matches_oracle(tmp_path, oracle_lib, bits):
     stream_d = [int(x[1], 16) for x in lines if x[0] == "stream"][0]
     want_long = int(oracle_lib.hash_long(ok, pay, nthreads=4))
     assert long_d == want_long and stream_d == want_long
+    assert [int(x[1], 16) for x in lines if x[0] == "longhost"] == [want_long]
+    assert [int(x[2], 16) for x in lines if x[0] == "tput"] == got_batch
     assert [int(x[1]) for x in lines if x[0] == "einval"] == [-1]
