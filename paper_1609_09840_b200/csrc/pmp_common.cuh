@@ -9,11 +9,15 @@ namespace pmp {
 
 constexpr uint32_t kShortMax = 127;      // bytes; k_short handles B <= kShortMax
 constexpr uint32_t kBigBytes = 1u << 16; // work-list class "big" (processed first)
+// k_short block shape (round-2 measurement, profiles/r02/s_block_shape_cmp.txt):
+// 15 consumer warps + the producer = 16 warps of 63 registers, two blocks per SM
+// (minBlocks 2: ptxas may use 64 registers), a 72 KB byte ring: configs[1]
+// 0.2805 -> 0.2765 ms against 16 consumer warps at 56 registers
 #ifndef PMP_SHORT_WARPS
-#define PMP_SHORT_WARPS 16
+#define PMP_SHORT_WARPS 15
 #endif
 #ifndef PMP_SHORT_RING_KB
-#define PMP_SHORT_RING_KB 64
+#define PMP_SHORT_RING_KB 72
 #endif
 constexpr int kShortWarps = PMP_SHORT_WARPS;  // consumer warps per k_short block (+1 producer)
 constexpr int kWWarps = 4;               // warps per k_wstring / k_node block

@@ -113,7 +113,10 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
 #if PMP_SHORT_DIAG >= 3
   constexpr int G = 4;
 #else
-  constexpr int G = V2 ? kShortG64 : 8;
+#ifndef PMP_SHORT_GD
+#define PMP_SHORT_GD 8
+#endif
+  constexpr int G = V2 ? kShortG64 : PMP_SHORT_GD;
 #endif
 #pragma unroll
   for (int tb = 0; tb < 16; tb += G) {
@@ -197,7 +200,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
 // tile whose span exceeds kSpanMaxTile is "direct": consumers read its short
 // strings from global.  Strings longer than kShortMax are appended by the
 // consumers to the work list of k_wstring in either mode.
-constexpr int kTile = 32 * kShortWarps;                        // 512 strings per tile (16 consumer warps)
+constexpr int kTile = 32 * kShortWarps;                        // 480 strings per tile (15 consumer warps)
 #ifndef PMP_SHORT_SLOTS
 #define PMP_SHORT_SLOTS 8
 #endif
@@ -245,10 +248,13 @@ __device__ unsigned long long g_trace_blk[1024][3];   // per block: smid, tiles 
 #endif
 
 // DUAL: BITS = 64 and a second, 32-bit schedule in K.a32 / K.b32 whose digests go to os2
-// (tuning builds: PMP_SHORT_MINB = min resident blocks for ptxas, PMP_SHORT_MAXNREG
-// = register cap; the product build sets neither: ptxas then lands at 56
-// registers, two 17-warp blocks per SM -- an explicit minBlocks of 1 gives 64
-// registers and ONE block per SM, 13% slower)
+// (PMP_SHORT_MINB = min resident blocks for ptxas: 2 in the product build, so
+// ptxas may take up to 64 registers for the 512-thread blocks while two fit
+// per SM; with 17-warp blocks an explicit minBlocks of 1 gave 64 registers and
+// ONE block per SM, 13% slower.  PMP_SHORT_MAXNREG: register cap, tuning only)
+#ifndef PMP_SHORT_MINB
+#define PMP_SHORT_MINB 2
+#endif
 template <int BITS, bool V2 = false, bool DUAL = false>
 #if defined(PMP_SHORT_MAXNREG)
 __global__ void __maxnreg__(PMP_SHORT_MAXNREG)

@@ -688,9 +688,11 @@ def test_entry_points_edge_cases(torch_dev, oracle_lib):
     assert pmp.pmp_hash_batch_multi([k64.handle], big.data_ptr(), d_off.data_ptr(), 3, [0], 0) == pmp.PMP_EINVAL
 
 
-@pytest.mark.parametrize("n", [511, 512, 513, 1024, 1025, 296 * 512 - 1, 296 * 512 + 1, 3 * 296 * 512 + 77])
+@pytest.mark.parametrize("n", [479, 480, 481, 960, 961, 4097, 296 * 480 - 1, 296 * 480 + 1, 3 * 296 * 480 + 77,
+                               296 * 512 + 1])
+@pytest.mark.usefixtures("batch_path")
 def test_short_tile_claims_at_tile_boundaries(torch_dev, oracle_lib, n):
-    """k_short claims its 512-string tiles dynamically (one global counter; a
+    """k_short claims its 480-string tiles dynamically (one global counter; a
     failed claim ends the block; single-width kernels claim one call ahead):
     string counts around tile multiples and beyond one tile per resident block
     hash every string exactly once -- fused two-width pass and both single
