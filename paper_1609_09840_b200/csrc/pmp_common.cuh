@@ -24,10 +24,10 @@ constexpr int kWWarps = 4;               // warps per k_wstring / k_node block
 constexpr uint32_t FULL = 0xffffffffu;
 // k_short word-loop granularity (words between warp-uniform exit tests)
 #ifndef PMP_SHORT_G64
-#define PMP_SHORT_G64 4
+#define PMP_SHORT_G64 2
 #endif
 #ifndef PMP_SHORT_G32
-#define PMP_SHORT_G32 8
+#define PMP_SHORT_G32 4
 #endif
 constexpr int kShortG64 = PMP_SHORT_G64, kShortG32 = PMP_SHORT_G32;
 

@@ -107,14 +107,14 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   macc_zero(A);
   Acc3 C = {0, 0, 0};
   uint32_t y0 = fetch(0);
-  // exit test granularity: the warp maximum is 7 or 8 full words for configs[1],
-  // so the tree pass tests once per 8 words (measured +0.9%; the two-level pass
-  // and the single-width kernels are faster with 4)
+  // exit test granularity (PMP_SHORT_GD): the warp maximum is 7 or 8 full words
+  // for configs[1]; with the 15-warp blocks a test every 4 words measured 1.2%
+  // faster than every 8 (round 1's 16-warp blocks: 8 was 0.9% faster)
 #if PMP_SHORT_DIAG >= 3
   constexpr int G = 4;
 #else
 #ifndef PMP_SHORT_GD
-#define PMP_SHORT_GD 8
+#define PMP_SHORT_GD 4   // exit test every 4 words (round 2, 15-warp blocks: -1.2% vs 8)
 #endif
   constexpr int G = V2 ? kShortG64 : PMP_SHORT_GD;
 #endif
