@@ -134,12 +134,18 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
       const bool f64 = t < tl64;
       const uint32_t lm = f64 ? lo : 0u, hm = f64 ? hi : 0u;
       if (t < 15) {
+#if PMP_SHORT_ORDER   // (tuning build: the PM+32 multiply-adds first)
+        mac32(C, K.a32[2 * t], lm);
+        mac32(C, K.a32[2 * t + 1], hm);
+        mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lm, hm);
+#else
 #if PMP_SHORT_DIAG != 7   // (diagnostic builds 6 / 7: one width's loop multiply-adds left out)
         mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lm, hm);  // Eq. (1)
 #endif
 #if PMP_SHORT_DIAG != 6
         mac32(C, K.a32[2 * t], lm);
         mac32(C, K.a32[2 * t + 1], hm);
+#endif
 #endif
       }
     }
@@ -202,7 +208,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
 // consumers to the work list of k_wstring in either mode.
 constexpr int kTile = 32 * kShortWarps;                        // 480 strings per tile (15 consumer warps)
 #ifndef PMP_SHORT_SLOTS
-#define PMP_SHORT_SLOTS 8
+#define PMP_SHORT_SLOTS 4   // round 2 (15-warp blocks): 4 slots, offsets 2 tiles ahead, -0.8% vs 8
 #endif
 #ifndef PMP_SHORT_OFF_AHEAD
 #define PMP_SHORT_OFF_AHEAD (PMP_SHORT_SLOTS / 2)
@@ -218,6 +224,9 @@ constexpr int kSlack = 144;                                    // fetch() reads 
 constexpr uint32_t kModeEnd = 2;
 #ifndef PMP_SHORT_DIAG
 #define PMP_SHORT_DIAG 0
+#endif
+#ifndef PMP_SHORT_ORDER
+#define PMP_SHORT_ORDER 0
 #endif
 struct TileHdr {
   uint64_t alo;    // global address of staged byte 0
