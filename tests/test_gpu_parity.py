@@ -715,3 +715,57 @@ def test_short_tile_claims_at_tile_boundaries(torch_dev, oracle_lib, n):
     assert np.array_equal(pmp.as_u64(o32), want32)
     assert np.array_equal(run_batch(torch_dev, k64, pay, off), want64)
     assert np.array_equal(run_batch(torch_dev, k32, pay, off), want32)
+
+
+def test_concurrent_calls_share_key_handles(torch_dev, oracle_lib):
+    """Key handles are shareable across threads and streams (S:174, S:269,
+    S:326): four host threads hash different batches (throughput path, latency
+    path, host-resident path, long string) with the SAME handles on their own
+    streams at once; every result equals the oracle's."""
+    import threading
+
+    import torch
+
+    k64, k32 = pmp.Keys.generate(71, 64), pmp.Keys.generate(72, 32)
+    rng = np.random.default_rng(71)
+    jobs = []
+    for j in range(4):
+        lens = rng.integers(0, 300, size=6000 if j % 2 == 0 else 1500).astype(np.uint64)
+        off = datagen.offsets_from_lengths(lens) + j
+        pay = datagen.payload_host(80 + j, 0, int(off[-1]))
+        jobs.append((off, pay))
+    long_data = datagen.payload_host(90, 0, 3 * 1024 * 128 + 11)
+    results, errors = {}, []
+
+    def work(j):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                off, pay = jobs[j]
+                if j == 2:
+                    results[j] = pmp.hash_batch_host([k64, k32], pay, off)
+                else:
+                    d_pay = torch.from_numpy(pay).to(torch_dev, non_blocking=False)
+                    d_off = torch.from_numpy(off.view(np.int64)).to(torch_dev)
+                    o64, o32 = pmp.hash_batch_multi([k64, k32], d_pay, d_off)
+                    st.synchronize()
+                    results[j] = (pmp.as_u64(o64), pmp.as_u64(o32))
+                if j == 3:
+                    d = torch.from_numpy(long_data).to(torch_dev)
+                    out = pmp.hash_long(k64, d, long_data.size)
+                    st.synchronize()
+                    results["long"] = int(pmp.as_u64(out)[0])
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    ths = [threading.Thread(target=work, args=(j,)) for j in range(4)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors
+    for j in range(4):
+        off, pay = jobs[j]
+        assert np.array_equal(results[j][0], oracle_batch(oracle_lib, 71, 64, pay, off)), j
+        assert np.array_equal(results[j][1], oracle_batch(oracle_lib, 72, 32, pay, off)), j
+    assert results["long"] == oracle_lib.hash_long(oracle_lib.keygen(71, 64), long_data, nthreads=NT)
