@@ -735,9 +735,10 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   if (cudaMemsetAsync(wcount, 0, 28, st) != cudaSuccess) return PMP_ECUDA;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    const void *fs[6] = {(const void *)k_short<64>, (const void *)k_short<32>, (const void *)k_short<64, true>,
+    const void *fs[8] = {(const void *)k_short<64>, (const void *)k_short<32>, (const void *)k_short<64, true>,
                          (const void *)k_short<32, true>, (const void *)k_short<64, false, true>,
-                         (const void *)k_short<64, true, true>};
+                         (const void *)k_short<64, true, true>, (const void *)k_short<64, false, false, true>,
+                         (const void *)k_short<32, false, false, true>};
     for (const void *f : fs) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kShortSmem);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
@@ -757,7 +758,12 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     offsets = (const uint64_t *)al;
   }
   // ---- short strings (and the work list of long ones)
-  const void *kshort = dual ? (v2 ? (const void *)k_short<64, true, true> : (const void *)k_short<64, false, true>)
+  // (buckets, os.M != 0: the instantiations with the bucket code; the hot ones store digests only)
+  const bool bkt = os.M != 0;
+  if (bkt && (dual || v2)) return PMP_EINVAL;
+  const void *kshort = bkt ? (k->bits == 64 ? (const void *)k_short<64, false, false, true>
+                                            : (const void *)k_short<32, false, false, true>)
+                     : dual ? (v2 ? (const void *)k_short<64, true, true> : (const void *)k_short<64, false, true>)
                             : v2 ? (k->bits == 64 ? (const void *)k_short<64, true> : (const void *)k_short<32, true>)
                                  : (k->bits == 64 ? (const void *)k_short<64> : (const void *)k_short<32>);
   const int threads = kShortThreads;  // consumers + producer (+ sorter) warps

@@ -261,7 +261,14 @@ template <> PMP_DI void store_digest<64>(void *out, uint64_t i, uint64_t lo) {
 template <> PMP_DI void store_digest<32>(void *out, uint64_t i, uint64_t lo) {
   reinterpret_cast<uint32_t *>(out)[i] = mix32((uint32_t)lo);
 }
-template <int BITS> PMP_DI void emit(const OutSpec &os, uint64_t i, uint64_t lo) {
+// BKT = false: digests only, the bucket code compiled out (the hot k_short
+// instantiations: a 64-bit modulo by a runtime M in the kernel costs the
+// configs[1] kernel 0.7% even when it never runs)
+template <int BITS, bool BKT = true> PMP_DI void emit(const OutSpec &os, uint64_t i, uint64_t lo) {
+  if constexpr (!BKT) {
+    store_digest<BITS>(os.out, i, lo);
+    return;
+  }
   if (os.M == 0) {
     store_digest<BITS>(os.out, i, lo);
     return;

@@ -264,7 +264,7 @@ __device__ unsigned long long g_trace_blk[1024][3];   // per block: smid, tiles 
 #ifndef PMP_SHORT_MINB
 #define PMP_SHORT_MINB 2
 #endif
-template <int BITS, bool V2 = false, bool DUAL = false>
+template <int BITS, bool V2 = false, bool DUAL = false, bool BKT = false>
 #if defined(PMP_SHORT_MAXNREG)
 __global__ void __maxnreg__(PMP_SHORT_MAXNREG)
 #elif defined(PMP_SHORT_MINB)
@@ -494,7 +494,9 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
 #endif
         if constexpr (DUAL) short_tree_dual<V2>(K, skeys, skeys32, B, 8 * (sofs & 3), tfm, fetch, lo, lo32);
         else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (sofs & 3), tfm, fetch);
-      } else {
+      }
+#if PMP_SHORT_DIAG != 10  // (diagnostic build 10: the direct-tile path compiled out, valid for configs[1] only)
+      else {
         // direct tile: read the string's aligned 32-bit words straight from global,
         // touching only words that overlap [start, end) (never past offsets[n]).
         const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
@@ -506,9 +508,10 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         if constexpr (DUAL) short_tree_dual<V2>(K, skeys, skeys32, B, 8 * (uint32_t)(sa & 3), tfm, fetch, lo, lo32);
         else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, fetch);
       }
+#endif
       if (valid) {
-        emit<BITS>(os, i, lo);
-        if constexpr (DUAL) emit<32>(os2, i, lo32);
+        emit<BITS, BKT>(os, i, lo);
+        if constexpr (DUAL) emit<32, BKT>(os2, i, lo32);
       }
     }
     __syncwarp();

@@ -72,8 +72,11 @@ struct WHdr {        // one per stage, written by the issuing lane
 };
 constexpr size_t kWSmemPerWarpBig =
     ((size_t)kWStages * (kWStageBytes + sizeof(WHdr) + 8) + sizeof(WStack) + 15) & ~(size_t)15;
+#ifndef PMP_M_STAGES
+#define PMP_M_STAGES 2
+#endif
 constexpr size_t kWSmemPerWarpMid =   // mid_phase's layout (kept in step with kMSmemPerWarp)
-    ((size_t)2 * (4 * (1024 + 32) + 4 * 32 + 8) + 15) & ~(size_t)15;
+    ((size_t)PMP_M_STAGES * (4 * (1024 + 32) + 4 * 32 + 8) + 15) & ~(size_t)15;
 constexpr size_t kWSmemPerWarp = kWSmemPerWarpBig > kWSmemPerWarpMid ? kWSmemPerWarpBig : kWSmemPerWarpMid;
 // block region: a_{2,0..127} (POLY: W[0..127] lo words), b_1..8, the key-only
 // values a_{2,r} * (b_1 + a_{1,0}) mod p (lo words, then hi bits) of a
