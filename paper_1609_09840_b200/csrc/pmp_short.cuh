@@ -110,7 +110,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   // exit test granularity (PMP_SHORT_GD): the warp maximum is 7 or 8 full words
   // for configs[1]; with the 15-warp blocks a test every 4 words measured 1.2%
   // faster than every 8 (round 1's 16-warp blocks: 8 was 0.9% faster)
-#if PMP_SHORT_DIAG >= 3
+#if PMP_SHORT_DIAG >= 3 && PMP_SHORT_DIAG <= 5   // (diagnostic builds 3-5: the loop capped, see below)
   constexpr int G = 4;
 #else
 #ifndef PMP_SHORT_GD
@@ -474,7 +474,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
       if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
     }
     // warp max of the number of full words (the marker word is handled apart)
-#if PMP_SHORT_DIAG >= 3  // diagnostic build: the word loop capped at 4 words (what padding costs); 5: no loop
+#if PMP_SHORT_DIAG >= 3 && PMP_SHORT_DIAG <= 5  // diagnostic builds: the word loop capped at 4 words (what padding costs); 5: no loop
     const int tfm = min(PMP_SHORT_DIAG == 5 ? 0 : 4, (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u));
 #else
     const int tfm = (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u);
@@ -494,9 +494,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
 #endif
         if constexpr (DUAL) short_tree_dual<V2>(K, skeys, skeys32, B, 8 * (sofs & 3), tfm, fetch, lo, lo32);
         else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (sofs & 3), tfm, fetch);
-      }
-#if PMP_SHORT_DIAG != 10  // (diagnostic build 10: the direct-tile path compiled out, valid for configs[1] only)
-      else {
+      } else {
         // direct tile: read the string's aligned 32-bit words straight from global,
         // touching only words that overlap [start, end) (never past offsets[n]).
         const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
@@ -508,7 +506,6 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
         if constexpr (DUAL) short_tree_dual<V2>(K, skeys, skeys32, B, 8 * (uint32_t)(sa & 3), tfm, fetch, lo, lo32);
         else lo = short_tree_lo<BITS, V2>(K, skeys, B, 8 * (uint32_t)(sa & 3), tfm, fetch);
       }
-#endif
       if (valid) {
         emit<BITS, BKT>(os, i, lo);
         if constexpr (DUAL) emit<32, BKT>(os2, i, lo32);
