@@ -304,7 +304,11 @@ __device__ PMP_MID_INLINE void mid_phase(const uint64_t *__restrict__ keys, cons
       // they were loaded into (its shared tail cost 16 register moves per half:
       // two-level fixed4k +3.4%); the tree variant measured 1% faster with
       // one shared tail.
+#ifdef PMP_M_DUPTAIL
+      constexpr bool kDupTail = PMP_M_DUPTAIL;
+#else
       constexpr bool kDupTail = POLY;
+#endif
       uint4 U[4];
       auto mac_half = [&](uint4 (&U)[4]) {
 #if PMP_M_DIAG  // diagnostic build: the mid-phase pipeline alone (units folded by XOR, no multiply-adds)
