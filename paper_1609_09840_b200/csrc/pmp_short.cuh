@@ -197,7 +197,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
     return;
   }
 #endif
-  if (up) mac32(C, skeys32[2 * tl64], zl);                   // the full PM+32 word 2 tl64
+  if (up) mac32(C, skeys32[2 * tl64], zl);                   // the full PM+32 word 2 tl64 (a select here: +0.3% slower)
   if (!V2 && tl64 == 0) {
     lo64 = w;                                                // |sigma| = 1 (reading Q2)
   } else {
