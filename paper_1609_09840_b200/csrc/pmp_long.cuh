@@ -12,7 +12,11 @@ namespace pmp {
 // is added once in k_combine, so V = C + sum over callers ("Long
 // strings: affine split").
 template <int BITS>
+#ifdef PMP_NODE_MINB   // (tuning build; an explicit minBlocks of 1 changes ptxas's choice: 123 -> 134 registers)
+__global__ void __launch_bounds__(kWWarps * 32, PMP_NODE_MINB)
+#else
 __global__ void __launch_bounds__(kWWarps * 32)
+#endif
 k_node(const uint64_t *__restrict__ keys, StrView s, uint64_t cb, uint64_t ce, uint64_t qb, uint64_t qe,
        int single, uint64_t *__restrict__ s2) {
   using T = Tr<BITS>;
