@@ -390,6 +390,14 @@ class Ctx:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
         return float(t.item())
 
+    def all_ok(self, ok):
+        """True on every rank iff `ok` on every rank (a failed rank must still
+        take part in the collectives that follow)."""
+        t = self.torch.tensor([1 if ok else 0], dtype=self.torch.int64, device=self.cdev)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+        return bool(t.item())
+
     def barrier(self):
         if self.world > 1:
             self.dist.barrier()
@@ -457,9 +465,15 @@ def prepare_long(args, wl, ctx, pmp, keys):
         partial / all-gather / combine.  Digest read back to the host."""
         if args.variant != "tree" or args.stream_mib:
             return None
-        h = torch.empty(hi - lo, dtype=torch.uint8, pin_memory=True)
-        h.copy_(d_full)
-        torch.cuda.synchronize()
+        err = None
+        try:
+            h = torch.empty(hi - lo, dtype=torch.uint8, pin_memory=True)
+            h.copy_(d_full)
+            torch.cuda.synchronize()
+        except Exception as ex:  # pinned host memory can run out on a shared node
+            err = repr(ex)[:200]
+        if not ctx.all_ok(err is None):
+            return {"value": None, "unit": "GB/s", "error": err or "another rank failed"}
         dig = np.zeros(1, dtype=np.uint64)
 
         def one():
@@ -549,26 +563,39 @@ def prepare_batch(args, wl, ctx, pmp, keys):
         """The same batch from pinned HOST memory through pmp_hash_batch_host
         (tree) -- pieces copied H2D, hashed and copied back D2H on 3 internal
         streams -- digests in host memory at the end of every step."""
-        h_pay = torch.empty(max(total_bytes, 1), dtype=torch.uint8, pin_memory=True)
-        h_pay[:total_bytes].copy_(d_pay[:total_bytes])
-        h_off = torch.from_numpy(offs.view(np.int64)).pin_memory()
-        h_out = {b: torch.empty(n, dtype=outs[b].dtype).pin_memory() for b in wl.bits}
-        torch.cuda.synchronize()
+        # several ranks of one node pin their host copies at once: above 8 GiB per
+        # rank, time a string-aligned prefix of the rank's strings (same rate, said so)
+        n_e, tb_e = n, total_bytes
+        cap = 8 << 30
+        if ctx.world > 1 and total_bytes > cap:
+            n_e = max(1, int(np.searchsorted(offs, np.uint64(cap), side="right")) - 1)
+            tb_e = int(offs[n_e])
+        err = None
+        try:
+            h_pay = torch.empty(max(tb_e, 1), dtype=torch.uint8, pin_memory=True)
+            h_pay[:tb_e].copy_(d_pay[:tb_e])
+            h_off = torch.from_numpy(offs[:n_e + 1].view(np.int64)).pin_memory()
+            h_out = {b: torch.empty(n_e, dtype=outs[b].dtype).pin_memory() for b in wl.bits}
+            torch.cuda.synchronize()
+        except Exception as ex:  # pinned host memory can run out on a shared node
+            err = repr(ex)[:200]
+        if not ctx.all_ok(err is None):
+            return {"value": None, "unit": "GB/s", "error": err or "another rank failed"}
         host_api = not v2
         d_out = outs
 
         def one():
             if host_api:
                 pmp._check(pmp.pmp_hash_batch_host([keys[b].handle for b in wl.bits], h_pay.data_ptr(),
-                                                   h_off.data_ptr(), n, [h_out[b].data_ptr() for b in wl.bits],
+                                                   h_off.data_ptr(), n_e, [h_out[b].data_ptr() for b in wl.bits],
                                                    args.e2e_piece_mib << 20, ctx.sp), "e2e hash")
                 return
-            d_pay[:total_bytes].copy_(h_pay[:total_bytes], non_blocking=True)
-            d_off.copy_(h_off, non_blocking=True)
+            d_pay[:tb_e].copy_(h_pay[:tb_e], non_blocking=True)
+            d_off[:n_e + 1].copy_(h_off, non_blocking=True)
             for b in wl.bits:
-                pmp._check(pmp.pmp_hash2_batch(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n,
+                pmp._check(pmp.pmp_hash2_batch(keys[b].handle, d_pay.data_ptr(), d_off.data_ptr(), n_e,
                                                d_out[b].data_ptr(), ctx.sp), "e2e hash")
-                h_out[b].copy_(d_out[b][:n], non_blocking=True)
+                h_out[b].copy_(d_out[b][:n_e], non_blocking=True)
 
         one()
         torch.cuda.synchronize()
@@ -580,11 +607,13 @@ def prepare_batch(args, wl, ctx, pmp, keys):
         ev1.record(ctx.stream)
         torch.cuda.synchronize()
         ms = ctx.max_over_ranks(ev0.elapsed_time(ev1) / steps)
-        moved = ctx.sum_over_ranks(total_bytes * len(wl.bits))
+        moved = ctx.sum_over_ranks(tb_e * len(wl.bits))
         del h_pay
         return {"value": moved / (ms / 1000) / 1e9, "unit": "GB/s",
-                "h2d_bytes_per_step": total_bytes + 8 * (n + 1),
-                "d2h_bytes_per_step": n * sum(b // 8 for b in wl.bits), "ms_per_step": ms,
+                "h2d_bytes_per_step": tb_e + 8 * (n_e + 1),
+                "d2h_bytes_per_step": n_e * sum(b // 8 for b in wl.bits), "ms_per_step": ms,
+                **({"sample": f"first {n_e} of the rank's {n} strings ({tb_e} B): pinned host memory of "
+                              f"{ctx.world} ranks per node"} if n_e < n else {}),
                 "path": (f"pmp_hash_batch_host (pinned host buffers, {'both widths in one pass, ' if fused else ''}"
                          f"{args.e2e_piece_mib or 64} MiB pieces: H2D / hash / D2H overlapped on 3 streams)" if host_api else
                          "pinned host -> cudaMemcpyAsync -> pmp_hash2_batch (both widths) -> host")}
