@@ -317,6 +317,16 @@ uint64_t pmp_launch_count(void);
  * the process-wide value and returns the previous one.  The two-level
  * variant always takes the throughput path. */
 uint64_t pmp_set_small_batch_max(uint64_t n);
+
+/* Short-string kernel of the throughput path (tuning / test hook).  1: the
+ * level-1 sums of strings of <= 64 bytes run as an exact u8 x u8 -> s32
+ * matrix product on the tensor cores (k_short_tc, tcgen05.mma kind::i8);
+ * 0: every short string takes k_short's per-thread word loop.  Both give
+ * identical digests.  Applies to the tree variant without buckets (the
+ * two-level variant and bucket mode always take k_short).  on < 0 only
+ * queries.  Default 1 (environment PMP_SHORT_TC=0 selects 0).  Returns the
+ * previous setting. */
+int pmp_set_short_tc(int on);
 void pmp_prof_enable(int on);
 void pmp_prof_reset(void);
 int pmp_prof_read(const char *prefix, double *ms, uint64_t *count);

@@ -73,6 +73,7 @@ def lib() -> ctypes.CDLL:
             "pmp_selftest": ([_int, _int, _vp, _u64, _vp, _vp], _int),
             "pmp_launch_count": ([], _u64),
             "pmp_set_small_batch_max": ([_u64], _u64),
+            "pmp_set_short_tc": ([ctypes.c_int], ctypes.c_int),
             "pmp_quality_collisions": ([_int, _u64, _u64, _vp, ctypes.c_uint32, _vp, ctypes.c_uint32, _vp, _vp, _vp,
                                         _vp], _int),
             "pmp_prof_enable": ([_int], None),
@@ -228,6 +229,12 @@ def pmp_launch_count() -> int:
 
 def pmp_set_small_batch_max(n: int) -> int:
     return int(lib().pmp_set_small_batch_max(n))
+
+
+def pmp_set_short_tc(on: int) -> int:
+    """1: short strings' level-1 sums on the tensor cores (k_short_tc), 0: the
+    word loop (k_short), -1: query.  Returns the previous setting."""
+    return int(lib().pmp_set_short_tc(int(on)))
 
 
 def pmp_prof_enable(on: bool) -> None:

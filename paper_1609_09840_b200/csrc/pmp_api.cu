@@ -140,6 +140,21 @@ int sm_count(int dev) {
 // ----------------------------------------------------------------- instrumentation
 std::atomic<uint64_t> g_launches{0};
 std::atomic<uint64_t> g_small_max{kSmallMax};  // batches of <= this many strings take k_small
+// short strings: 1 = k_short_tc (the level-1 sum on the tensor cores) for the
+// tree variant without buckets, 0 = k_short's word loop; -1 = not chosen yet
+// (environment PMP_SHORT_TC, default 0 while the tensor-core kernel is not faster)
+std::atomic<int> g_short_tc{-1};
+static bool use_short_tc() {
+  int v = g_short_tc.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char *e = getenv("PMP_SHORT_TC");
+    v = (e && e[0] == '1') ? 1 : 0;
+    int expect = -1;
+    g_short_tc.compare_exchange_strong(expect, v);
+    v = g_short_tc.load(std::memory_order_relaxed);
+  }
+  return v != 0;
+}
 std::atomic<int> g_prof{0};
 struct ProfRec {
   std::string name;
@@ -684,9 +699,34 @@ static int resident_blocks(const void *f, int threads, size_t smem, const char *
   int b = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, threads, smem);
   if (b < 1) b = 1;
-  if (getenv("PMP_VERBOSE")) fprintf(stderr, "pmp: %s smem %zu B, %d blocks/SM\n", name, smem, b);
+  if (getenv("PMP_VERBOSE")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, f);
+    fprintf(stderr, "pmp: %s smem %zu B, %d blocks/SM (regs %d, static smem %zu, max dyn smem %d, carveout %d)\n",
+            name, smem, b, fa.numRegs, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes,
+            fa.preferredShmemCarveout);
+  }
   cache.push_back({f, b});
   return b;
+}
+
+// Resident blocks per SM of k_short_tc from its resources (registers, shared
+// memory, threads, TMEM columns).
+static int tc_resident_blocks(const void *f, int threads, size_t smem, int device) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return 1;
+  int smem_sm = 0, regs_sm = 0, thr_sm = 0;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, device);
+  const int warps = (threads + 31) / 32;
+  const int regs_warp = ((fa.numRegs * 32 + 255) / 256) * 256;
+  int b = (int)(smem_sm / (smem + fa.sharedSizeBytes + 1024));
+  b = std::min(b, regs_sm / std::max(1, regs_warp * warps));
+  b = std::min(b, thr_sm / threads);
+  b = std::min(b, (int)(512 / kTcTmemCols));
+  if (getenv("PMP_VERBOSE")) fprintf(stderr, "pmp: k_short_tc %d blocks/SM from its resources\n", b);
+  return std::max(b, 1);
 }
 
 // One batch under schedule k (digests to os) and, for the dual-width fused
@@ -747,6 +787,12 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
                          (const void *)k_wstring<32, true>, (const void *)k_wstring_dual<false>,
                          (const void *)k_wstring_dual<true>};
     for (const void *f : ws) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWSmem);
+    const void *ts[3] = {(const void *)k_short_tc<64, true>, (const void *)k_short_tc<64, false>,
+                         (const void *)k_short_tc<32, false>};
+    for (const void *f : ts) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    }
   });
   // the offsets ring is fed by TMA bulk copies, which need 16-byte aligned sources
   if ((uintptr_t)offsets & 15) {
@@ -766,15 +812,31 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
                      : dual ? (v2 ? (const void *)k_short<64, true, true> : (const void *)k_short<64, false, true>)
                             : v2 ? (k->bits == 64 ? (const void *)k_short<64, true> : (const void *)k_short<32, true>)
                                  : (k->bits == 64 ? (const void *)k_short<64> : (const void *)k_short<32>);
-  const int threads = kShortThreads;  // consumers + producer (+ sorter) warps
-  uint64_t grid = (n + kTile - 1) / kTile;
-  const uint64_t maxgrid = (uint64_t)sms * resident_blocks(kshort, threads, kShortSmem, "k_short");  // persistent grid
+  // (tree variant, digests: the tensor-core kernel, k_short_tc)
+  const bool tcp = !bkt && !v2 && use_short_tc();
+  const void *kshort_tc = dual ? (const void *)k_short_tc<64, true>
+                               : (k->bits == 64 ? (const void *)k_short_tc<64, false> : (const void *)k_short_tc<32, false>);
+  const void *ks = tcp ? kshort_tc : kshort;
+  const int threads = tcp ? kTcThreads : kShortThreads;  // consumers + producer warps
+  const size_t smem = tcp ? kTcSmem : kShortSmem;
+  const uint64_t tile = tcp ? (uint64_t)kTcTile : (uint64_t)kTile;
+  uint64_t grid = (n + tile - 1) / tile;
+  int rb = resident_blocks(ks, threads, smem, tcp ? "k_short_tc" : "k_short");
+  if (tcp) {
+    // the occupancy calculator reports 1 block/SM for this kernel (it uses
+    // TMEM); registers, shared memory and TMEM columns (512 per SM, kTcTmemCols
+    // per block) admit 2, and 2 co-reside (measured: 0.336 -> 0.266 ms)
+    static const int rb_tc = tc_resident_blocks(ks, threads, smem, k->device);
+    rb = rb_tc;
+    if (const char *e = getenv("PMP_TC_BLOCKS")) rb = atoi(e) > 0 ? atoi(e) : rb;   // (tuning)
+  }
+  const uint64_t maxgrid = (uint64_t)sms * rb;  // persistent grid
   if (grid > maxgrid) grid = maxgrid;
   const OutSpec o2 = dual ? *os2 : os;
-  int rc = launch("k_short", st, [&] {
+  int rc = launch(tcp ? "k_short_tc" : "k_short", st, [&] {
     void *args[] = {(void *)&pk, (void *)&bytes, (void *)&offsets, (void *)&n, (void *)&os, (void *)&wlist,
                     (void *)&wcount, (void *)&o2};
-    cudaLaunchKernel(kshort, dim3((unsigned)grid), dim3(threads), args, kShortSmem, st);
+    cudaLaunchKernel(ks, dim3((unsigned)grid), dim3(threads), args, smem, st);
   });
   if (rc) return rc;
   // ---- long strings: warp per big string, 8-lane group per mid string (persistent
@@ -1217,6 +1279,11 @@ int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_
 uint64_t pmp_launch_count(void) { return g_launches.load(); }
 
 uint64_t pmp_set_small_batch_max(uint64_t n) { return g_small_max.exchange(n); }
+int pmp_set_short_tc(int on) {
+  const int prev = use_short_tc() ? 1 : 0;
+  if (on >= 0) g_short_tc.store(on ? 1 : 0);
+  return prev;
+}
 
 #if PMP_SHORT_TRACE
 // diagnostic builds only: the k_short clock64 timeline (pmp_short.cuh)

@@ -16,6 +16,8 @@
 //   pmp_stream.cuh   incremental hashing with device-resident level state
 //   pmp_misc.cuh     self-test hooks, the hash-table histogram pass
 //   pmp_small.cuh    k_small: the latency path for small batches (one launch)
+//   pmp_short_tc.cuh k_short_tc: strings <= 64 bytes, the level-1 sum as an
+//                    exact u8 x u8 -> s32 product on the tensor cores (tcgen05)
 //   pmp_poly.cuh     (included by pmp_api.cu) long strings, two-level variant
 //
 // Citations: P:n = PAPER.md line n.  Eq. (1); Algorithm 1 P:427-443;
@@ -29,3 +31,4 @@
 #include "pmp_stream.cuh"
 #include "pmp_misc.cuh"
 #include "pmp_small.cuh"
+#include "pmp_short_tc.cuh"

@@ -29,13 +29,17 @@ def torch_dev():
     return torch.device("cuda:0")
 
 
-@pytest.fixture(params=["throughput", "latency"])
+@pytest.fixture(params=["tensor", "wordloop", "latency"])
 def batch_path(request, torch_dev):
-    """Run a batch test through the throughput path (k_short + k_wstring) and
-    through the latency path (k_small, batches of <= 4096 strings)."""
-    prev = pmp.pmp_set_small_batch_max(0 if request.param == "throughput" else 4096)
+    """Run a batch test through the throughput path with short strings on the
+    tensor cores (k_short_tc + k_wstring), with short strings in the word loop
+    (k_short + k_wstring), and through the latency path (k_small, batches of
+    <= 4096 strings)."""
+    prev = pmp.pmp_set_small_batch_max(4096 if request.param == "latency" else 0)
+    prev_tc = pmp.pmp_set_short_tc(1 if request.param == "tensor" else 0)
     yield request.param
     pmp.pmp_set_small_batch_max(prev)
+    pmp.pmp_set_short_tc(prev_tc)
 
 
 def _u(bits):
