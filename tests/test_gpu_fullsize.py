@@ -95,26 +95,36 @@ def test_hashtable_full_size_every_hash(dev, oracle_lib):
     """configs[1] in bench.py's launch configuration: 2^24 strings U[8,64] B,
     seed 2, both widths in one fused pass (pmp_hash_batch_multi).  EVERY digest
     of both widths equals the oracle's, and so do the per-width launches
-    (pmp_hash_batch, the k_short single-width kernels)."""
+    (pmp_hash_batch, the k_short single-width kernels) -- with the word loop
+    (k_short) and with the level-1 sums on the tensor cores (k_short_tc)."""
     import torch
 
     wl = datagen.WORKLOADS["hashtable"]
     offs = datagen.offsets_from_lengths(wl.lengths())
     pay, d_off = _device_batch(dev, wl.seed, offs)
     k64, k32 = pmp.Keys.generate(wl.seed, 64), pmp.Keys.generate(wl.seed, 32)
-    o64, o32 = pmp.hash_batch_multi([k64, k32], pay, d_off)
-    s64 = pmp.hash_batch(k64, pay, d_off)
-    s32 = pmp.hash_batch(k32, pay, d_off)
-    torch.cuda.synchronize()
-    g64, g32 = pmp.as_u64(o64), pmp.as_u64(o32)
+    got = {}
+    prev = pmp.pmp_set_short_tc(0)
+    try:
+        for tc in (0, 1):   # the word loop (k_short, default) and the tensor-core kernel (k_short_tc)
+            pmp.pmp_set_short_tc(tc)
+            o64, o32 = pmp.hash_batch_multi([k64, k32], pay, d_off)
+            s64 = pmp.hash_batch(k64, pay, d_off)
+            s32 = pmp.hash_batch(k32, pay, d_off)
+            torch.cuda.synchronize()
+            got[tc] = [pmp.as_u64(x) for x in (o64, s64, o32, s32)]
+    finally:
+        pmp.pmp_set_short_tc(prev)
     del pay
     torch.cuda.empty_cache()
     w64 = _oracle_all(oracle_lib, oracle_lib.keygen(wl.seed, 64), wl.seed, offs)
-    _assert_all_equal(g64, w64, 64)
-    _assert_all_equal(pmp.as_u64(s64), w64, 64)
     w32 = _oracle_all(oracle_lib, oracle_lib.keygen(wl.seed, 32), wl.seed, offs)
-    _assert_all_equal(g32, w32, 32)
-    _assert_all_equal(pmp.as_u64(s32), w32, 32)
+    for tc in (0, 1):
+        g64, s64, g32, s32 = got[tc]
+        _assert_all_equal(g64, w64, 64)
+        _assert_all_equal(s64, w64, 64)
+        _assert_all_equal(g32, w32, 32)
+        _assert_all_equal(s32, w32, 32)
 
 
 def test_fixed4k_full_size_every_hash(dev, oracle_lib):
