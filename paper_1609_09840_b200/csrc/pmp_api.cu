@@ -688,28 +688,6 @@ static void launch_pdl(const void *f, unsigned grid, unsigned threads, void **ar
   cudaLaunchKernelExC(&cfg, f, args);
 }
 
-// Resident blocks per SM of a kernel (registers, shared memory), cached: the
-// persistent grids are exactly one wave.
-static int resident_blocks(const void *f, int threads, size_t smem, const char *name) {
-  static std::mutex mu;
-  static std::vector<std::pair<const void *, int>> cache;
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto &e : cache)
-    if (e.first == f) return e.second;
-  int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, threads, smem);
-  if (b < 1) b = 1;
-  if (getenv("PMP_VERBOSE")) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, f);
-    fprintf(stderr, "pmp: %s smem %zu B, %d blocks/SM (regs %d, static smem %zu, max dyn smem %d, carveout %d)\n",
-            name, smem, b, fa.numRegs, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes,
-            fa.preferredShmemCarveout);
-  }
-  cache.push_back({f, b});
-  return b;
-}
-
 // Resident blocks per SM of k_short_tc from its resources (registers, shared
 // memory, threads, TMEM columns).
 static int tc_resident_blocks(const void *f, int threads, size_t smem, int device) {
@@ -727,6 +705,33 @@ static int tc_resident_blocks(const void *f, int threads, size_t smem, int devic
   b = std::min(b, (int)(512 / kTcTmemCols));
   if (getenv("PMP_VERBOSE")) fprintf(stderr, "pmp: k_short_tc %d blocks/SM from its resources\n", b);
   return std::max(b, 1);
+}
+
+// Resident blocks per SM of a kernel (registers, shared memory), cached per
+// kernel: the persistent grids are exactly one wave.  tc_device >= 0: the
+// tensor-core kernel, counted from its resources -- the occupancy calculator
+// reports 1 block/SM for it (it uses TMEM); registers, shared memory and TMEM
+// columns (512 per SM, kTcTmemCols per block) admit 2, and 2 co-reside
+// (measured: 0.336 -> 0.266 ms on configs[1]).
+static int resident_blocks(const void *f, int threads, size_t smem, const char *name, int tc_device = -1) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void *, int>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &e : cache)
+    if (e.first == f) return e.second;
+  int b = 0;
+  if (tc_device >= 0) b = tc_resident_blocks(f, threads, smem, tc_device);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, f, threads, smem);
+  if (b < 1) b = 1;
+  if (getenv("PMP_VERBOSE")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, f);
+    fprintf(stderr, "pmp: %s smem %zu B, %d blocks/SM (regs %d, static smem %zu, max dyn smem %d, carveout %d)\n",
+            name, smem, b, fa.numRegs, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes,
+            fa.preferredShmemCarveout);
+  }
+  cache.push_back({f, b});
+  return b;
 }
 
 // One batch under schedule k (digests to os) and, for the dual-width fused
@@ -821,15 +826,9 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   const size_t smem = tcp ? kTcSmem : kShortSmem;
   const uint64_t tile = tcp ? (uint64_t)kTcTile : (uint64_t)kTile;
   uint64_t grid = (n + tile - 1) / tile;
-  int rb = resident_blocks(ks, threads, smem, tcp ? "k_short_tc" : "k_short");
-  if (tcp) {
-    // the occupancy calculator reports 1 block/SM for this kernel (it uses
-    // TMEM); registers, shared memory and TMEM columns (512 per SM, kTcTmemCols
-    // per block) admit 2, and 2 co-reside (measured: 0.336 -> 0.266 ms)
-    static const int rb_tc = tc_resident_blocks(ks, threads, smem, k->device);
-    rb = rb_tc;
+  int rb = resident_blocks(ks, threads, smem, tcp ? "k_short_tc" : "k_short", tcp ? k->device : -1);
+  if (tcp)
     if (const char *e = getenv("PMP_TC_BLOCKS")) rb = atoi(e) > 0 ? atoi(e) : rb;   // (tuning)
-  }
   const uint64_t maxgrid = (uint64_t)sms * rb;  // persistent grid
   if (grid > maxgrid) grid = maxgrid;
   const OutSpec o2 = dual ? *os2 : os;
