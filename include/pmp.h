@@ -324,8 +324,9 @@ uint64_t pmp_set_small_batch_max(uint64_t n);
  * 0: every short string takes k_short's per-thread word loop.  Both give
  * identical digests.  Applies to the tree variant without buckets (the
  * two-level variant and bucket mode always take k_short).  on < 0 only
- * queries.  Default 1 (environment PMP_SHORT_TC=0 selects 0).  Returns the
- * previous setting. */
+ * queries.  Default 0: the tensor-core kernel is bit-exact but not faster
+ * on configs[1]; the environment PMP_SHORT_TC=1 selects
+ * 1.  Returns the previous setting. */
 int pmp_set_short_tc(int on);
 void pmp_prof_enable(int on);
 void pmp_prof_reset(void);
