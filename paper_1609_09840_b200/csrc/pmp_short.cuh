@@ -132,13 +132,14 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   Acc3 C = {0, 0, 0};
   uint32_t y0 = fetch(0);
   // exit test granularity (PMP_SHORT_GD): the warp maximum is 7 or 8 full words
-  // for configs[1]; with the 15-warp blocks a test every 4 words measured 1.2%
-  // faster than every 8 (round 1's 16-warp blocks: 8 was 0.9% faster)
+  // for configs[1]; every 8 words measured 0.4% faster than every 4 on the
+  // final round-2 code (stable to 0.1% with the bench's head start), 5% faster
+  // than every 2 (profiles/r02/s_knobs_final.txt)
 #if PMP_SHORT_DIAG >= 3 && PMP_SHORT_DIAG <= 5   // (diagnostic builds 3-5: the loop capped, see below)
   constexpr int G = 4;
 #else
 #ifndef PMP_SHORT_GD
-#define PMP_SHORT_GD 4   // exit test every 4 words (round 2, 15-warp blocks: -1.2% vs 8)
+#define PMP_SHORT_GD 8   // exit test every 8 words (final round-2 code: 0.2649 vs 0.2660 ms for 4, 0.2787 for 2)
 #endif
   constexpr int G = V2 ? kShortG64 : PMP_SHORT_GD;
 #endif
