@@ -9,15 +9,16 @@ namespace pmp {
 
 constexpr uint32_t kShortMax = 127;      // bytes; k_short handles B <= kShortMax
 constexpr uint32_t kBigBytes = 1u << 16; // work-list class "big" (processed first)
-// k_short block shape (round-2 measurement, profiles/r02/s_block_shape_cmp.txt):
-// 15 consumer warps + the producer = 16 warps of 63 registers, two blocks per SM
-// (minBlocks 2: ptxas may use 64 registers), a 72 KB byte ring: configs[1]
-// 0.2805 -> 0.2765 ms against 16 consumer warps at 56 registers
+// k_short block shape (round-2 measurements, profiles/r02/s_block_shape_w31.txt):
+// ONE block per SM of 31 consumer warps + the producer (1024 threads, 63
+// registers) with a 160 KB byte ring and 992-string tiles: configs[1]
+// 0.2650 -> 0.2555 ms against two blocks of 15 + 1 warps with 72 KB rings
+// (29 / 27 consumer warps: 0.2716 / 0.2585; a 128 KB ring 0.2655)
 #ifndef PMP_SHORT_WARPS
-#define PMP_SHORT_WARPS 15
+#define PMP_SHORT_WARPS 31
 #endif
 #ifndef PMP_SHORT_RING_KB
-#define PMP_SHORT_RING_KB 72
+#define PMP_SHORT_RING_KB 160
 #endif
 constexpr int kShortWarps = PMP_SHORT_WARPS;  // consumer warps per k_short block (+1 producer)
 constexpr int kWWarps = 4;               // warps per k_wstring / k_node block

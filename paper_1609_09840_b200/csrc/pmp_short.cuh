@@ -246,7 +246,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
 // tile whose span exceeds kSpanMaxTile is "direct": consumers read its short
 // strings from global.  Strings longer than kShortMax are appended by the
 // consumers to the work list of k_wstring in either mode.
-constexpr int kTile = 32 * kShortWarps;                        // 480 strings per tile (15 consumer warps)
+constexpr int kTile = 32 * kShortWarps;                        // 992 strings per tile (31 consumer warps)
 #ifndef PMP_SHORT_SLOTS
 #define PMP_SHORT_SLOTS 4   // round 2 (15-warp blocks): 4 slots, offsets 2 tiles ahead, -0.8% vs 8
 #endif
@@ -258,8 +258,11 @@ constexpr uint32_t kByteRing = PMP_SHORT_RING_KB * 1024;
 // (Length sorting / partitioning of the tiles, to cut the zero-padding
 // multiply-adds, was measured five ways in round 1 and with a dedicated sorter
 // warp in round 2 -- 2x slower: profiles/r01f, profiles/r02/README.md.)
-constexpr uint32_t kSpanMaxTile = kByteRing / 2 < 32 * 1024 ? kByteRing / 2 : 32 * 1024;  // larger spans go direct
-constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 3088
+#ifndef PMP_SHORT_SPAN_KB
+#define PMP_SHORT_SPAN_KB 64   // staged tiles up to 64 KB (992 strings of 8..64 B: ~36 KB)
+#endif
+constexpr uint32_t kSpanMaxTile = kByteRing / 2 < PMP_SHORT_SPAN_KB * 1024 ? kByteRing / 2 : PMP_SHORT_SPAN_KB * 1024;  // larger spans go direct
+constexpr int kOffBytes = ((kTile + 1) * 8 + 15) & ~15;        // 7952
 constexpr int kSlack = 144;                                    // fetch() reads <= 136 B past a start
 constexpr uint32_t kModeEnd = 2;
 #ifndef PMP_SHORT_DIAG
@@ -294,12 +297,11 @@ __device__ unsigned long long g_trace_blk[1024][3];   // per block: smid, tiles 
 #endif
 
 // DUAL: BITS = 64 and a second, 32-bit schedule in K.a32 / K.b32 whose digests go to os2
-// (PMP_SHORT_MINB = min resident blocks for ptxas: 2 in the product build, so
-// ptxas may take up to 64 registers for the 512-thread blocks while two fit
-// per SM; with 17-warp blocks an explicit minBlocks of 1 gave 64 registers and
-// ONE block per SM, 13% slower.  PMP_SHORT_MAXNREG: register cap, tuning only)
+// (PMP_SHORT_MINB = min resident blocks for ptxas: 1 for the product's
+// 1024-thread block (<= 64 registers either way); the earlier 512-thread
+// shape used 2.  PMP_SHORT_MAXNREG: register cap, tuning only)
 #ifndef PMP_SHORT_MINB
-#define PMP_SHORT_MINB 2
+#define PMP_SHORT_MINB 1
 #endif
 template <int BITS, bool V2 = false, bool DUAL = false, bool BKT = false>
 #if defined(PMP_SHORT_MAXNREG)
