@@ -56,7 +56,10 @@ constexpr int kWTile = 4096;
 #endif
 constexpr int kWStages = PMP_W_STAGES;
 constexpr int kWStageBytes = kWTile + 32;      // + 16 B overlap + 16 B read slack
-constexpr int kWBlockWarps = 4;
+#ifndef PMP_W_BLOCK_WARPS
+#define PMP_W_BLOCK_WARPS 4
+#endif
+constexpr int kWBlockWarps = PMP_W_BLOCK_WARPS;
 struct WStack {      // lane 0's streaming state for levels 3..8
   uint64_t T[kL + 1];
   uint64_t pushed[kL - 2];
