@@ -19,8 +19,9 @@
 // 15 + 7 diagonals into the exact S (shifts and adds) and reduce it as before.
 // This moves the ~50 IMAD.WIDE per string of the word loop (k_short, the
 // kernel's bound: profiles/r02/README.md) onto the tensor cores -- but the row
-// pass costs about as much as they did (measured: 0.266 against k_short's
-// 0.265 ms on configs[1]), so this kernel is an option
+// pass costs about as much as they did (measured on configs[1]: 0.266 ms
+// against k_short's 0.265 at the same two-block shape, and k_short's one-block
+// shape reaches 0.2555), so this kernel is an option
 // (pmp_set_short_tc), bit-exact and tested, not the default.
 //
 // Strings of 65..127 bytes in these tiles take k_short's word loop (the same
