@@ -68,7 +68,40 @@ PMP_DI void macc_zero(MacAcc64 &A) {
 // A += a * s  (a, s < 2^64).  One IMAD.WIDE.U32 (carry out) per 32x32 partial
 // product plus carry-counter updates (IADD3.X / IMAD.X); the four partial
 // products go to four independent accumulators (no serial dependence inside a word).
+#ifndef PMP_MAC_ORDER
+// 1: the two products of s0, then the two of s1 (the shared operand stays in
+// the operand reuse cache): configs[1] k_short 0.2555 -> 0.2548 ms, configs[2]
+// k_wstring 0.7356 -> 0.7285, long string neutral, two-level configs[1] +1%
+// (profiles/r02/s_mac_order.txt)
+#define PMP_MAC_ORDER 1
+#endif
 PMP_DI void mac64(MacAcc64 &A, uint32_t a0, uint32_t a1, uint32_t s0, uint32_t s1) {
+#if PMP_MAC_ORDER
+  asm("{\n\t.reg .u32 l0, l1, m0, m1, n0, n1, h0, h1;\n\t"
+      "mov.b64 {l0, l1}, %0;\n\t"
+      "mov.b64 {m0, m1}, %1;\n\t"
+      "mov.b64 {n0, n1}, %2;\n\t"
+      "mov.b64 {h0, h1}, %3;\n\t"
+      "mad.lo.cc.u32  l0, %8, %10, l0;\n\t"
+      "madc.hi.cc.u32 l1, %8, %10, l1;\n\t"
+      "addc.u32       %4, %4, 0;\n\t"
+      "mad.lo.cc.u32  n0, %9, %10, n0;\n\t"
+      "madc.hi.cc.u32 n1, %9, %10, n1;\n\t"
+      "addc.u32       %6, %6, 0;\n\t"
+      "mad.lo.cc.u32  m0, %8, %11, m0;\n\t"
+      "madc.hi.cc.u32 m1, %8, %11, m1;\n\t"
+      "addc.u32       %5, %5, 0;\n\t"
+      "mad.lo.cc.u32  h0, %9, %11, h0;\n\t"
+      "madc.hi.cc.u32 h1, %9, %11, h1;\n\t"
+      "addc.u32       %7, %7, 0;\n\t"
+      "mov.b64 %0, {l0, l1};\n\t"
+      "mov.b64 %1, {m0, m1};\n\t"
+      "mov.b64 %2, {n0, n1};\n\t"
+      "mov.b64 %3, {h0, h1};\n\t}"
+      : "+l"(A.L), "+l"(A.M), "+l"(A.N), "+l"(A.H), "+r"(A.cL), "+r"(A.cM), "+r"(A.cN), "+r"(A.cH)
+      : "r"(a0), "r"(a1), "r"(s0), "r"(s1));
+  return;
+#endif
   asm("{\n\t.reg .u32 l0, l1, m0, m1, n0, n1, h0, h1;\n\t"
       "mov.b64 {l0, l1}, %0;\n\t"
       "mov.b64 {m0, m1}, %1;\n\t"
