@@ -763,7 +763,7 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   }
   if (!v2 && n <= g_small_max.load(std::memory_order_relaxed)) {
     // latency path: one launch, no scratch, no work list (pmp_small.cuh)
-    const unsigned grid = (unsigned)((n + kSmallThreads - 1) / kSmallThreads);
+    const unsigned grid = (unsigned)((n + kSmallPer - 1) / kSmallPer);
     const uint64_t *b1 = k->d_blob, *b2 = dual ? k2->d_blob : k->d_blob;
     const OutSpec o2 = dual ? *os2 : os;
     return launch("k_small", st, [&] {

@@ -11,15 +11,26 @@ namespace pmp {
 // no host-side work besides the launch: the throughput path (k_short's TMA
 // pipeline, a zeroed work list, k_wstring) costs ~20 us of fixed latency that
 // dominates a call of a few thousand strings (BASELINE configs[0]: 1,000).
-//   - one thread per string; a string of <= kShortMax bytes is hashed straight
-//     from global memory by the same word loop as k_short (short_tree_lo /
-//     short_tree_dual, the `direct` fetch: aligned 32-bit loads of the words
-//     overlapping the string, never past its end);
+//   - a block takes kSmallPer consecutive strings, one lane of its warp 0 each;
+//     a string of <= kShortMax bytes is hashed straight from global memory by
+//     the same word loop as k_short (short_tree_lo / short_tree_dual, the
+//     `direct` fetch: aligned 32-bit loads of the words overlapping the
+//     string, never past its end);
 //   - longer strings are listed in shared memory and hashed afterwards by the
 //     block's warps, one warp per string: level-2 nodes by the warp chunk
 //     engine (warp_chunks), levels >= 3 streamed bottom-up.
+//     (Round 2 had 256 strings per block, so a small batch of long strings got
+//     one warp per 32 of them: 4,096 x 64 KiB took 568 us, 1,024 x 256 KiB
+//     2,044 us; tools/small_batches.py, profiles/r02/small_batches.txt.)
 constexpr int kSmallThreads = 256;
 constexpr uint64_t kSmallMax = 4096;   // strings per call routed here (pmp_api.cu)
+// strings per block: so that every long string of a small batch gets a warp of
+// its own (a block's 8 warps), not one warp per 32 of them
+#ifndef PMP_SMALL_PER
+#define PMP_SMALL_PER 8
+#endif
+constexpr int kSmallPer = PMP_SMALL_PER;
+static_assert(kSmallPer >= 1 && kSmallPer <= 32, "warp 0 lists the block's strings");
 
 // V mod 2^n of one string of B > kShortMax bytes hashed by one warp (every
 // lane returns the value).  Keys from the device blob (b[8], a[8][128]).
@@ -77,43 +88,47 @@ k_small(const ParamKeys K, const uint64_t *__restrict__ blob, const uint64_t *__
         const OutSpec os2) {
   __shared__ uint64_t skeys[32];
   __shared__ uint32_t skeys32[32];
-  __shared__ uint32_t longs[kSmallThreads];
+  __shared__ uint32_t longs[kSmallPer];
   __shared__ uint32_t nlong;
-  const int lane = threadIdx.x & 31;
-  if (threadIdx.x < 32) {
-    skeys[threadIdx.x] = K.a[threadIdx.x];
-    if (DUAL) skeys32[threadIdx.x] = K.a32[threadIdx.x];
-  }
-  if (threadIdx.x == 0) nlong = 0;
-  __syncthreads();
-  const uint64_t i = (uint64_t)blockIdx.x * kSmallThreads + threadIdx.x;
-  const bool valid = i < n;
-  const uint64_t o0 = valid ? offsets[i] : 0, B64 = valid ? offsets[i + 1] - o0 : 0;
-  const bool is_short = valid && B64 <= kShortMax;
-  if (valid && !is_short) longs[atomicAdd(&nlong, 1u)] = (uint32_t)i;
-  const uint32_t B = is_short ? (uint32_t)B64 : 0u;
-  const int tfm = (int)__reduce_max_sync(FULL, B / (BITS / 8));
-  if (is_short) {
-    const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
-    const uintptr_t pa = sa & ~(uintptr_t)3;
-    auto fetch = [&](int kk) {
-      const uintptr_t a = pa + 4 * (uintptr_t)kk;
-      return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
-    };
-    const uint32_t sh = 8 * (uint32_t)(sa & 3);
-    if constexpr (DUAL) {
-      uint64_t lo;
-      uint32_t lo32;
-      short_tree_dual<false>(K, skeys, skeys32, B, sh, tfm, fetch, lo, lo32);
-      emit<64>(os, i, lo);
-      emit<32>(os2, i, lo32);
-    } else {
-      emit<BITS>(os, i, short_tree_lo<BITS, false>(K, skeys, B, sh, tfm, fetch));
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (wib == 0) {
+    // warp 0: the block's kSmallPer strings, one lane each; the short ones are
+    // hashed here, the long ones listed for the block's warps
+    skeys[lane] = K.a[lane];
+    if (DUAL) skeys32[lane] = K.a32[lane];
+    __syncwarp();
+    const uint64_t i = (uint64_t)blockIdx.x * kSmallPer + lane;
+    const bool valid = lane < kSmallPer && i < n;
+    const uint64_t o0 = valid ? offsets[i] : 0, B64 = valid ? offsets[i + 1] - o0 : 0;
+    const bool is_short = valid && B64 <= kShortMax;
+    const unsigned lm = __ballot_sync(FULL, valid && !is_short);
+    if (lane == 0) nlong = (uint32_t)__popc(lm);
+    if (valid && !is_short) longs[__popc(lm & ((1u << lane) - 1))] = (uint32_t)i;
+    const uint32_t B = is_short ? (uint32_t)B64 : 0u;
+    const int tfm = (int)__reduce_max_sync(FULL, B / (BITS / 8));
+    if (is_short) {
+      const uintptr_t sa = (uintptr_t)(bytes + o0), se = sa + B;
+      const uintptr_t pa = sa & ~(uintptr_t)3;
+      auto fetch = [&](int kk) {
+        const uintptr_t a = pa + 4 * (uintptr_t)kk;
+        return (B > 0 && a < se) ? ld_u32(reinterpret_cast<const void *>(a)) : 0u;
+      };
+      const uint32_t sh = 8 * (uint32_t)(sa & 3);
+      if constexpr (DUAL) {
+        uint64_t lo;
+        uint32_t lo32;
+        short_tree_dual<false>(K, skeys, skeys32, B, sh, tfm, fetch, lo, lo32);
+        emit<64>(os, i, lo);
+        emit<32>(os2, i, lo32);
+      } else {
+        emit<BITS>(os, i, short_tree_lo<BITS, false>(K, skeys, B, sh, tfm, fetch));
+      }
     }
   }
   __syncthreads();
-  const int nw = kSmallThreads / 32;
-  for (uint32_t j = threadIdx.x >> 5; j < nlong; j += nw) {
+  // the block's long strings, one warp each (at most ceil(kSmallPer / 8) per warp)
+  constexpr int nw = kSmallThreads / 32;
+  for (uint32_t j = (uint32_t)wib; j < nlong; j += nw) {
     const uint32_t si = longs[j];
     const uint64_t a0 = offsets[si], len = offsets[si + 1] - a0;
     if constexpr (DUAL) {
