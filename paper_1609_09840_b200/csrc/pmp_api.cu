@@ -763,13 +763,17 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
   }
   if (!v2 && n <= g_small_max.load(std::memory_order_relaxed)) {
     // latency path: one launch, no scratch, no work list (pmp_small.cuh)
-    const unsigned grid = (unsigned)((n + kSmallPer - 1) / kSmallPer);
+    // strings per block: kSmallPer, or fewer for batches that do not fill ~2
+    // blocks per SM, so the spare warps split long strings (pmp_split.cuh)
+    const uint64_t per = std::min<uint64_t>(kSmallPer, std::max<uint64_t>(1, (n + 2 * sms - 1) / (2 * sms)));
+    const unsigned grid = (unsigned)((n + per - 1) / per);
+    const uint32_t per32 = (uint32_t)per;
     const uint64_t *b1 = k->d_blob, *b2 = dual ? k2->d_blob : k->d_blob;
     const OutSpec o2 = dual ? *os2 : os;
     return launch("k_small", st, [&] {
-      if (dual) k_small<64, true><<<grid, kSmallThreads, 0, st>>>(pk, b1, b2, bytes, offsets, n, os, o2);
-      else if (k->bits == 64) k_small<64, false><<<grid, kSmallThreads, 0, st>>>(pk, b1, b2, bytes, offsets, n, os, o2);
-      else k_small<32, false><<<grid, kSmallThreads, 0, st>>>(pk, b1, b2, bytes, offsets, n, os, o2);
+      if (dual) k_small<64, true><<<grid, kSmallThreads, 0, st>>>(pk, b1, b2, bytes, offsets, n, os, o2, per32);
+      else if (k->bits == 64) k_small<64, false><<<grid, kSmallThreads, 0, st>>>(pk, b1, b2, bytes, offsets, n, os, o2, per32);
+      else k_small<32, false><<<grid, kSmallThreads, 0, st>>>(pk, b1, b2, bytes, offsets, n, os, o2, per32);
     });
   }
   Scratch sc(st), sc_off(st);

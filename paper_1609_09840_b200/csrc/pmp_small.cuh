@@ -3,6 +3,7 @@
 #pragma once
 #include "pmp_engine.cuh"
 #include "pmp_short.cuh"
+#include "pmp_split.cuh"
 
 namespace pmp {
 
@@ -24,8 +25,10 @@ namespace pmp {
 //     2,044 us; tools/small_batches.py, profiles/r02/small_batches.txt.)
 constexpr int kSmallThreads = 256;
 constexpr uint64_t kSmallMax = 4096;   // strings per call routed here (pmp_api.cu)
-// strings per block: so that every long string of a small batch gets a warp of
-// its own (a block's 8 warps), not one warp per 32 of them
+// strings per block (at most): so that every long string of a small batch gets
+// a warp of its own (a block's 8 warps), not one warp per 32 of them.  Fewer
+// when the batch is small (pmp_api.cu: about two blocks per SM), so that the
+// spare warps of a block split its long strings (pmp_split.cuh)
 #ifndef PMP_SMALL_PER
 #define PMP_SMALL_PER 8
 #endif
@@ -85,20 +88,20 @@ template <int BITS, bool DUAL>
 __global__ void __launch_bounds__(kSmallThreads)
 k_small(const ParamKeys K, const uint64_t *__restrict__ blob, const uint64_t *__restrict__ blob32,
         const uint8_t *__restrict__ bytes, const uint64_t *__restrict__ offsets, uint64_t n, const OutSpec os,
-        const OutSpec os2) {
+        const OutSpec os2, uint32_t per) {
   __shared__ uint64_t skeys[32];
   __shared__ uint32_t skeys32[32];
   __shared__ uint32_t longs[kSmallPer];
   __shared__ uint32_t nlong;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   if (wib == 0) {
-    // warp 0: the block's kSmallPer strings, one lane each; the short ones are
-    // hashed here, the long ones listed for the block's warps
+    // warp 0: the block's `per` (<= kSmallPer) strings, one lane each; the
+    // short ones are hashed here, the long ones listed for the block's warps
     skeys[lane] = K.a[lane];
     if (DUAL) skeys32[lane] = K.a32[lane];
     __syncwarp();
-    const uint64_t i = (uint64_t)blockIdx.x * kSmallPer + lane;
-    const bool valid = lane < kSmallPer && i < n;
+    const uint64_t i = (uint64_t)blockIdx.x * per + lane;
+    const bool valid = lane < (int)per && i < n;
     const uint64_t o0 = valid ? offsets[i] : 0, B64 = valid ? offsets[i + 1] - o0 : 0;
     const bool is_short = valid && B64 <= kShortMax;
     const unsigned lm = __ballot_sync(FULL, valid && !is_short);
@@ -126,22 +129,87 @@ k_small(const ParamKeys K, const uint64_t *__restrict__ blob, const uint64_t *__
     }
   }
   __syncthreads();
-  // the block's long strings, one warp each (at most ceil(kSmallPer / 8) per warp)
+  const uint32_t nl = nlong;
+  if (nl == 0) return;
   constexpr int nw = kSmallThreads / 32;
-  for (uint32_t j = (uint32_t)wib; j < nlong; j += nw) {
-    const uint32_t si = longs[j];
-    const uint64_t a0 = offsets[si], len = offsets[si + 1] - a0;
-    if constexpr (DUAL) {
-      const uint64_t lo = warp_hash_string<64>(blob, bytes + a0, len, lane);
-      const uint64_t lo32 = warp_hash_string<32>(blob32, bytes + a0, len, lane);
-      if (lane == 0) {
-        emit<64>(os, si, lo);
-        emit<32>(os2, si, lo32);
+  if (nl >= (uint32_t)nw) {
+    // the block's long strings, one warp each
+    for (uint32_t j = (uint32_t)wib; j < nl; j += nw) {
+      const uint32_t si = longs[j];
+      const uint64_t a0 = offsets[si], len = offsets[si + 1] - a0;
+      if constexpr (DUAL) {
+        const uint64_t lo = warp_hash_string<64>(blob, bytes + a0, len, lane);
+        const uint64_t lo32 = warp_hash_string<32>(blob32, bytes + a0, len, lane);
+        if (lane == 0) {
+          emit<64>(os, si, lo);
+          emit<32>(os2, si, lo32);
+        }
+      } else {
+        const uint64_t lo = warp_hash_string<BITS>(blob, bytes + a0, len, lane);
+        if (lane == 0) emit<BITS>(os, si, lo);
       }
-    } else {
-      const uint64_t lo = warp_hash_string<BITS>(blob, bytes + a0, len, lane);
-      if (lane == 0) emit<BITS>(os, si, lo);
     }
+    return;
+  }
+  // fewer long strings than warps: string js = w mod nl gets the nsub warps
+  // w = js, js + nl, ...; a string of several level-2 nodes is split over them
+  // by the affine identity (pmp_split.cuh: each warp sums W(q) v2'(q) over
+  // every nsub-th node, the first warp adds the partials and C(T)), the others
+  // are hashed by their first warp alone
+  __shared__ uint64_t spart[nw][2][2];   // per warp and schedule: partial (lo, hi)
+  const uint32_t js = (uint32_t)wib % nl, sub = (uint32_t)wib / nl, nsub = (nw - 1 - js) / nl + 1;
+  const uint32_t si = longs[js];
+  const uint64_t a0 = offsets[si], len = offsets[si + 1] - a0;
+  const StrView sv = whole_string(bytes + a0, len);
+  auto split_of = [&](int bits, Geom &gm) {
+    gm = make_geom(len / (uint64_t)(bits / 8) + 1);
+    return nsub > 1 && gm.leff >= 2 && gm.T[2] > 1;
+  };
+  auto part = [&](auto tag, const uint64_t *kb, int sch) {   // this warp's partial, or the whole digest
+    constexpr int B2 = decltype(tag)::value;
+    using Fe = typename Tr<B2>::Fe;
+    Geom gm;
+    if (split_of(B2, gm)) {
+      const Fe v = strided_partial<B2>(kb, sv, gm, sub, nsub, lane);
+      uint64_t w2[2];
+      fe_store(w2, v);
+      if (lane == 0) {
+        spart[wib][sch][0] = w2[0];
+        spart[wib][sch][1] = w2[1];
+      }
+    } else if (sub == 0) {
+      const uint64_t lo = warp_hash_string<B2>(kb, bytes + a0, len, lane);
+      if (lane == 0) emit<B2>(sch ? os2 : os, si, lo);
+    }
+  };
+  auto combine = [&](auto tag, const uint64_t *kb, int sch) {  // first warp of a split string: V = C(T) + sum
+    constexpr int B2 = decltype(tag)::value;
+    using Acc = typename Tr<B2>::Acc;
+    using Fe = typename Tr<B2>::Fe;
+    Geom gm;
+    if (sub != 0 || !split_of(B2, gm)) return;
+    Acc x;
+    acc_zero(x);
+    acc_add_fe(x, key_only_constant<B2>(kb, gm, lane));
+    for (uint32_t k = 0; k < nsub; k++) {
+      Fe v;
+      fe_load(&spart[js + k * nl][sch][0], v);
+      acc_add_fe(x, v);
+    }
+    if (lane == 0) emit<B2>(sch ? os2 : os, si, fe_lo(acc_reduce(x)));
+  };
+  if constexpr (DUAL) {
+    part(std::integral_constant<int, 64>(), blob, 0);
+    part(std::integral_constant<int, 32>(), blob32, 1);
+  } else {
+    part(std::integral_constant<int, BITS>(), blob, 0);
+  }
+  __syncthreads();
+  if constexpr (DUAL) {
+    combine(std::integral_constant<int, 64>(), blob, 0);
+    combine(std::integral_constant<int, 32>(), blob32, 1);
+  } else {
+    combine(std::integral_constant<int, BITS>(), blob, 0);
   }
 }
 

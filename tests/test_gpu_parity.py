@@ -591,6 +591,44 @@ def test_long_host_streaming(torch_dev, oracle_lib, bits):
         assert pmp.hash_long_host(keys, data, piece_bytes=5 * cb) == want, total   # pageable host memory
 
 
+@pytest.mark.parametrize("nlong", [1, 2, 3, 5, 7, 8])
+def test_small_batch_long_strings_split(torch_dev, oracle_lib, nlong):
+    """Latency path (k_small, 8 strings per block): a block with fewer long
+    strings than warps splits each multi-node string over its spare warps by
+    the affine identity (V = C(T) + sum_q W(q) v2'(q), C(T) on the device,
+    pmp_split.cuh); 8 long strings take one warp each.  Sizes around level-2
+    node edges, strings with a level-3 and level-4 tree, misaligned starts;
+    both widths and the fused two-schedule call, equal to the oracle."""
+    import torch
+
+    rng = np.random.default_rng(nlong)
+    prev = pmp.pmp_set_small_batch_max(4096)
+    try:
+        cands = [128 * 1024 * 2 + 5, 128 * 1024 * 3 - 1, 128 * 1024 + 1, 128 * 512 * 5 + 17, 1_000_003,
+                 128 * 1024 * 128 + 1024 + 3, 128 * 512 * 129 + 7, 128 * 1024 - 1, 400_000]
+        for rep in range(2):
+            longs = list(rng.choice(cands, size=nlong, replace=False)) if rep == 0 else list(cands[:nlong])
+            lens = np.array(longs + list(rng.integers(0, 128, size=8 - nlong)) + [3, 200_000, 9], dtype=np.uint64)
+            perm = rng.permutation(8)
+            lens[:8] = lens[:8][perm]
+            off = datagen.offsets_from_lengths(lens) + int(rng.integers(0, 16))
+            pay = datagen.payload_host(60 + nlong, 0, int(off[-1]))
+            d_pay = torch.from_numpy(pay).to(torch_dev)
+            d_off = torch.from_numpy(off.view(np.int64)).to(torch_dev)
+            k64, k32 = pmp.Keys.generate(61, 64), pmp.Keys.generate(62, 32)
+            w64 = oracle_batch(oracle_lib, 61, 64, pay, off)
+            w32 = oracle_batch(oracle_lib, 62, 32, pay, off)
+            s64, s32 = pmp.hash_batch(k64, d_pay, d_off), pmp.hash_batch(k32, d_pay, d_off)
+            m64, m32 = pmp.hash_batch_multi([k64, k32], d_pay, d_off)
+            torch.cuda.synchronize()
+            for name, o, w in (("64", s64, w64), ("32", s32, w32), ("dual64", m64, w64), ("dual32", m32, w32)):
+                got = pmp.as_u64(o)
+                bad = np.nonzero(got != w)[0]
+                assert bad.size == 0, (name, rep, [(int(i), int(lens[i])) for i in bad[:8]])
+    finally:
+        pmp.pmp_set_small_batch_max(prev)
+
+
 @pytest.mark.parametrize("order", [(64, 32), (32, 64), (64, 64, 32), (32,)])
 @pytest.mark.usefixtures("batch_path")
 def test_multi_schedule_fused_pass(torch_dev, oracle_lib, order):
