@@ -318,6 +318,19 @@ uint64_t pmp_launch_count(void);
  * variant always takes the throughput path. */
 uint64_t pmp_set_small_batch_max(uint64_t n);
 
+/* Huge strings in a batch (tuning / test hook).  The throughput path hashes a
+ * string of >= `bytes` bytes node-parallel (k_huge: parts of 128 KiB
+ * claimed by every warp of a persistent grid, combined by the affine identity
+ * of DESIGN.md section 7 with the key-only constant computed on the device)
+ * instead of with one warp; at most `cap` such strings per call (the rest
+ * keep the one-warp path).  Identical digests either way.  Defaults: 4 MiB,
+ * 65,536.  pmp_set_huge_min(0) only queries; values below 64 KiB act as
+ * 64 KiB.  pmp_set_huge_cap(0) turns the huge path off.  Both set the
+ * process-wide value and return the previous one.  The two-level variant and
+ * the tensor-core short-string option keep the one-warp path. */
+uint64_t pmp_set_huge_min(uint64_t bytes);
+uint32_t pmp_set_huge_cap(uint32_t cap);
+
 /* Short-string kernel of the throughput path (tuning / test hook).  1: the
  * level-1 sums of strings of <= 64 bytes run as an exact u8 x u8 -> s32
  * matrix product on the tensor cores (k_short_tc, tcgen05.mma kind::i8);

@@ -74,6 +74,8 @@ def lib() -> ctypes.CDLL:
             "pmp_launch_count": ([], _u64),
             "pmp_set_small_batch_max": ([_u64], _u64),
             "pmp_set_short_tc": ([ctypes.c_int], ctypes.c_int),
+            "pmp_set_huge_min": ([ctypes.c_uint64], ctypes.c_uint64),
+            "pmp_set_huge_cap": ([ctypes.c_uint32], ctypes.c_uint32),
             "pmp_quality_collisions": ([_int, _u64, _u64, _vp, ctypes.c_uint32, _vp, ctypes.c_uint32, _vp, _vp, _vp,
                                         _vp], _int),
             "pmp_prof_enable": ([_int], None),
@@ -229,6 +231,16 @@ def pmp_launch_count() -> int:
 
 def pmp_set_small_batch_max(n: int) -> int:
     return int(lib().pmp_set_small_batch_max(n))
+
+
+def pmp_set_huge_min(nbytes: int) -> int:
+    """Throughput path: strings of >= nbytes go node-parallel (k_huge); 0 queries."""
+    return int(lib().pmp_set_huge_min(int(nbytes)))
+
+
+def pmp_set_huge_cap(cap: int) -> int:
+    """At most cap huge strings per call take k_huge (0: off).  Returns the previous cap."""
+    return int(lib().pmp_set_huge_cap(int(cap)))
 
 
 def pmp_set_short_tc(on: int) -> int:

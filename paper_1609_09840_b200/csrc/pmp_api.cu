@@ -140,6 +140,13 @@ int sm_count(int dev) {
 // ----------------------------------------------------------------- instrumentation
 std::atomic<uint64_t> g_launches{0};
 std::atomic<uint64_t> g_small_max{kSmallMax};  // batches of <= this many strings take k_small
+// throughput path: strings of >= g_huge_min bytes (at most g_huge_cap per call)
+// are hashed node-parallel by k_huge instead of one warp each (pmp_huge.cuh)
+#ifndef PMP_HUGE_MIN_DEFAULT
+#define PMP_HUGE_MIN_DEFAULT (4ull << 20)
+#endif
+std::atomic<uint64_t> g_huge_min{PMP_HUGE_MIN_DEFAULT};
+std::atomic<uint32_t> g_huge_cap{65536};
 // short strings: 1 = k_short_tc (the level-1 sum on the tensor cores) for the
 // tree variant without buckets, 0 = k_short's word loop; -1 = not chosen yet
 // (environment PMP_SHORT_TC, default 0 while the tensor-core kernel is not faster)
@@ -208,6 +215,8 @@ ParamKeys param_keys(const pmp_keys *k) {
   pk.b = k->b[0];
   pk.r = k->a[kM];  // a_{2,1}
   pk.b2 = k->b[1];
+  pk.huge_min = ~0ull;   // (the throughput path sets its own, hash_batch_impl)
+  pk.huge_cap = 0;
   return pk;
 }
 
@@ -777,11 +786,17 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
     });
   }
   Scratch sc(st), sc_off(st);
-  // work list (n u32) + counters [mid, big, then per schedule: next big, next mid batch; k_short tile claims]
-  if (sc.alloc((size_t)n * 4 + 32)) return PMP_ENOMEM;
+  // counters [mid, big, then per schedule: next big, next mid batch; k_short
+  // tile claims; huge capacity, slots and parts; part cursors] + work list (n u32) + huge list
+  // and states (pmp_huge_list.cuh; the two-level variant has none)
+  const uint64_t huge_min = v2 ? ~0ull : std::max<uint64_t>(g_huge_min.load(), kBigBytes);
+  const uint32_t huge_cap = v2 ? 0u : (uint32_t)std::min<uint64_t>(n, g_huge_cap.load());
+  pk.huge_min = huge_cap ? huge_min : ~0ull;
+  pk.huge_cap = huge_cap;
+  if (sc.alloc((size_t)(kWHeader + n + huge_cap) * 4 + 16 + (size_t)huge_cap * kHugeState * 8)) return PMP_ENOMEM;
   uint32_t *wcount = (uint32_t *)sc.p;
-  uint32_t *wlist = wcount + 8;
-  if (cudaMemsetAsync(wcount, 0, 28, st) != cudaSuccess) return PMP_ECUDA;
+  uint32_t *wlist = wcount + kWHeader;
+  if (cudaMemsetAsync(wcount, 0, kWHeader * 4, st) != cudaSuccess) return PMP_ECUDA;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
     const void *fs[8] = {(const void *)k_short<64>, (const void *)k_short<32>, (const void *)k_short<64, true>,
@@ -855,17 +870,36 @@ static int hash_batch_impl(const pmp_keys *k, const uint8_t *bytes, const uint64
       launch_pdl(kw, wgrid, kWBlockWarps * 32, args, kWSmem, st);
     });
   };
-  if (!dual) return launch_w(k, os);
+  // ---- huge strings (k_short's huge list), node-parallel; returns at once when empty
+  auto launch_h = [&]() -> int {
+    if (!huge_cap || tcp) return 0;   // (k_short_tc keeps every long string on the work list)
+    const void *kh = dual ? (const void *)k_huge<64, true>
+                          : (k->bits == 64 ? (const void *)k_huge<64, false> : (const void *)k_huge<32, false>);
+    const unsigned hgrid = (unsigned)(sms * resident_blocks(kh, kHugeThreads, 0, "k_huge"));
+    const uint64_t *hb1 = k->d_blob, *hb2 = dual ? k2->d_blob : k->d_blob;
+    const OutSpec ho2 = dual ? *os2 : os;
+    return launch("k_huge", st, [&] {
+      void *args[] = {(void *)&hb1, (void *)&hb2, (void *)&bytes, (void *)&offsets, (void *)&n, (void *)&os,
+                      (void *)&ho2, (void *)&wlist, (void *)&wcount};
+      launch_pdl(kh, hgrid, kHugeThreads, args, 0, st);
+    });
+  };
+  if (!dual) {
+    if (int rc2 = launch_w(k, os)) return rc2;
+    return launch_h();
+  }
   // both schedules over the shared work list in one launch (half the blocks each)
   const void *kw = v2 ? (const void *)k_wstring_dual<true> : (const void *)k_wstring_dual<false>;
   const unsigned wgrid = (unsigned)(2 * ((sms * resident_blocks(kw, kWBlockWarps * 32, kWSmem, "k_wstring") + 1) / 2));
   const uint64_t *b64 = k->d_blob, *b32 = k2->d_blob;
   const OutSpec o32 = *os2;
-  return launch("k_wstring", st, [&] {
+  rc = launch("k_wstring", st, [&] {
     void *args[] = {(void *)&b64, (void *)&b32, (void *)&bytes, (void *)&offsets, (void *)&n, (void *)&os,
                     (void *)&o32, (void *)&wlist, (void *)&wcount};
     launch_pdl(kw, wgrid, kWBlockWarps * 32, args, kWSmem, st);
   });
+  if (rc) return rc;
+  return launch_h();
 }
 
 int pmp_hash_batch(const pmp_keys *k, const uint8_t *bytes, const uint64_t *offsets, uint64_t n,
@@ -1282,6 +1316,8 @@ int pmp_selftest(int out_bits, int mode, const uint64_t *in, uint64_t n, uint64_
 uint64_t pmp_launch_count(void) { return g_launches.load(); }
 
 uint64_t pmp_set_small_batch_max(uint64_t n) { return g_small_max.exchange(n); }
+uint64_t pmp_set_huge_min(uint64_t bytes) { return bytes ? g_huge_min.exchange(bytes) : g_huge_min.load(); }
+uint32_t pmp_set_huge_cap(uint32_t cap) { return g_huge_cap.exchange(cap); }
 int pmp_set_short_tc(int on) {
   const int prev = use_short_tc() ? 1 : 0;
   if (on >= 0) g_short_tc.store(on ? 1 : 0);

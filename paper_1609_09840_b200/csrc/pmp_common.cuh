@@ -42,6 +42,10 @@ struct ParamKeys {
   uint32_t a32[32];
   uint64_t b32;
   uint64_t r32, b2_32;  // and its two-level r = a_{2,1}, b_2
+  // throughput path: strings of >= huge_min bytes go to the huge list (at most
+  // huge_cap of them; pmp_huge.cuh); huge_min = ~0: none
+  uint64_t huge_min;
+  uint32_t huge_cap;
 };
 
 // ------------------------------------------------------------- key-generation contract

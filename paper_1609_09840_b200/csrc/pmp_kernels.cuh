@@ -16,6 +16,7 @@
 //   pmp_stream.cuh   incremental hashing with device-resident level state
 //   pmp_misc.cuh     self-test hooks, the hash-table histogram pass
 //   pmp_split.cuh    one string's tree split over warps (affine split, C(T) on the device)
+//   pmp_huge.cuh     k_huge: strings of many MiB in a batch, parts claimed grid-wide
 //   pmp_small.cuh    k_small: the latency path for small batches (one launch)
 //   pmp_short_tc.cuh k_short_tc: strings <= 64 bytes, the level-1 sum as an
 //                    exact u8 x u8 -> s32 product on the tensor cores (tcgen05)
@@ -33,4 +34,5 @@
 #include "pmp_misc.cuh"
 #include "pmp_split.cuh"
 #include "pmp_small.cuh"
+#include "pmp_huge.cuh"
 #include "pmp_short_tc.cuh"

@@ -2,6 +2,7 @@
 // (part of the kernels included by pmp_kernels.cuh; citations as there)
 #pragma once
 #include "pmp_common.cuh"
+#include "pmp_huge_list.cuh"
 
 namespace pmp {
 
@@ -332,6 +333,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
   if (threadIdx.x < 32) skeys[threadIdx.x] = K.a[threadIdx.x];
   if (DUAL && threadIdx.x < 32) skeys32[threadIdx.x] = K.a32[threadIdx.x];
   if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) wcount[7] = K.huge_cap;   // for k_huge (pmp_huge_list.cuh)
     for (int q = 0; q < kRing; q++) {
       mbar_init(&bar_off[q], 1);
       mbar_init(&bar_done[q], kShortWarps);
@@ -498,9 +500,27 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     uint32_t B = (uint32_t)Bl;
     const unsigned longmask = __ballot_sync(FULL, is_long);
     if (longmask) {
-      // warp-aggregated append: big strings from the back, others from the front
-      const bool big = is_long && Bl >= kBigBytes;
-      const unsigned bigmask = __ballot_sync(FULL, big), midmask = longmask & ~bigmask;
+      const unsigned lt = (1u << lane) - 1;
+      // huge strings (>= K.huge_min bytes) to the huge list (huge_pool) while it
+      // has room (pmp_huge.cuh); the others: warp-aggregated append, big
+      // strings from the back, others from the front
+      const bool huge = is_long && Bl >= K.huge_min;
+      const unsigned hugemask = __ballot_sync(FULL, huge);
+      bool listed = is_long;
+      if (hugemask) {
+        uint32_t hbase = 0;
+        if (lane == 0) hbase = atomicAdd(&wcount[8], (uint32_t)__popc(hugemask));
+        hbase = __shfl_sync(FULL, hbase, 0);
+        const uint32_t slot = hbase + __popc(hugemask & lt);
+        if (huge && slot < K.huge_cap) {
+          uint32_t np = (uint32_t)huge_parts_of<BITS>(Bl);
+          if constexpr (DUAL) np = max(np, (uint32_t)huge_parts_of<32>(Bl));
+          huge_append(wlist, n, K.huge_cap, slot, (uint32_t)i, np);
+          listed = false;
+        }
+      }
+      const bool big = listed && Bl >= kBigBytes;
+      const unsigned bigmask = __ballot_sync(FULL, big), midmask = __ballot_sync(FULL, listed) & ~bigmask;
       uint32_t mbase = 0, bbase = 0;
       if (lane == 0) {
         if (midmask) mbase = atomicAdd(&wcount[0], (uint32_t)__popc(midmask));
@@ -508,8 +528,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
       }
       mbase = __shfl_sync(FULL, mbase, 0);
       bbase = __shfl_sync(FULL, bbase, 0);
-      const unsigned lt = (1u << lane) - 1;
-      if (is_long && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
+      if (listed && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
       if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
     }
     // warp max of the number of full words (the marker word is handled apart)

@@ -16,17 +16,18 @@ namespace pmp {
 // value with every v_1 = 0 (keys only).  The host computes the same C(T) for
 // pmp_hash_long_combine (pmp_api.cu, long_constant).
 
-// W(q) v2'(q) for level-2 node q (warp-collective; every lane returns it).
+// W(q) v2'(q) for level-2 node q of a string of T1 level-1 blocks and L_eff
+// levels (warp-collective; every lane returns it).
 template <int BITS>
-PMP_DI typename Tr<BITS>::Fe node_term(const uint64_t *__restrict__ keys, const StrView &s, const Geom &gm, uint64_t q,
-                                       const LaneKeys<BITS> &lk, int lane) {
+PMP_DI typename Tr<BITS>::Fe node_term(const uint64_t *__restrict__ keys, const StrView &s, uint64_t T1, int leff,
+                                       uint64_t q, const LaneKeys<BITS> &lk, int lane) {
   using Fe = typename Tr<BITS>::Fe;
   const uint64_t *bk = keys, *ak = keys + kL;
-  const uint64_t ce = min(128 * q + 128, gm.T[1]);
+  const uint64_t ce = min(128 * q + 128, T1);
   const ChunkOut<BITS> co = warp_chunks<BITS, false, true>(s, 128 * q, ce, lk, bk[0], ak + kM, lane);
   Fe v = acc_reduce(co.acc2);
   uint64_t d = q;
-  for (int j = 3; j <= gm.leff; j++) {
+  for (int j = 3; j <= leff; j++) {
     v = fe_mul(fe_from_word(ak[(uint64_t)(j - 1) * kM + (d & 127)], (Fe *)nullptr), v);
     d >>= 7;
   }
@@ -92,7 +93,7 @@ PMP_DI typename Tr<BITS>::Fe strided_partial(const uint64_t *__restrict__ keys, 
   lk.load(keys + kL, lane & 7);
   Acc x;
   acc_zero(x);
-  for (uint64_t q = first; q < gm.T[2]; q += step) acc_add_fe(x, node_term<BITS>(keys, s, gm, q, lk, lane));
+  for (uint64_t q = first; q < gm.T[2]; q += step) acc_add_fe(x, node_term<BITS>(keys, s, gm.T[1], gm.leff, q, lk, lane));
   return acc_reduce(x);
 }
 

@@ -469,6 +469,9 @@ __device__ __forceinline__ void wstring_body(const uint64_t *__restrict__ keys, 
   // launched with programmatic dependent launch after k_short (pmp_api.cu): the
   // work list is k_short's output, so wait for that grid (and its memory) first
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // k_huge (programmatic dependent launch after this grid) may be scheduled
+  // now: its blocks take what this persistent grid leaves free and wait there
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t nmid = wcount[0], nbig = wcount[1];
   if (nmid + nbig == 0) return;
   for (int k = threadIdx.x; k < (int)kM; k += blockDim.x) {

@@ -629,6 +629,51 @@ def test_small_batch_long_strings_split(torch_dev, oracle_lib, nlong):
         pmp.pmp_set_small_batch_max(prev)
 
 
+@pytest.mark.parametrize("cap", [65536, 2])
+def test_huge_strings_throughput_path(torch_dev, oracle_lib, cap):
+    """Throughput path with the huge threshold lowered to 64 KiB: long strings
+    go to k_huge (parts of 128 KiB claimed grid-wide, exact sums by atomics,
+    C(T) added by the warp finishing the last part; pmp_huge.cuh), at most
+    `cap` of them per call (the rest stay on k_wstring's big list).  Sizes at
+    level-2 node edges of both widths, level-3 and level-4 trees, misaligned
+    starts, mixed with short and mid strings; single schedules, the fused
+    two-schedule call and bucket mode, equal to the oracle."""
+    import torch
+
+    rng = np.random.default_rng(cap)
+    prev = (pmp.pmp_set_small_batch_max(0), pmp.pmp_set_huge_min(64 << 10), pmp.pmp_set_huge_cap(cap))
+    try:
+        big = [64 << 10, (128 << 10) - 1, 128 << 10, (128 << 10) + 1, (512 << 10) + 3, 1_000_003,
+               (128 << 20) // 8 + 1024 + 3, (64 << 10) * 129 + 7, 300_000]
+        lens = np.concatenate([rng.integers(0, 128, size=3000), rng.integers(128, 60000, size=200), big])
+        lens = lens.astype(np.uint64)
+        rng.shuffle(lens)
+        off = datagen.offsets_from_lengths(lens) + 5
+        pay = datagen.payload_host(70, 0, int(off[-1]))
+        d_pay = torch.from_numpy(pay).to(torch_dev)
+        d_off = torch.from_numpy(off.view(np.int64)).to(torch_dev)
+        k64, k32 = pmp.Keys.generate(71, 64), pmp.Keys.generate(72, 32)
+        w64 = oracle_batch(oracle_lib, 71, 64, pay, off)
+        w32 = oracle_batch(oracle_lib, 72, 32, pay, off)
+        s64, s32 = pmp.hash_batch(k64, d_pay, d_off), pmp.hash_batch(k32, d_pay, d_off)
+        m64, m32 = pmp.hash_batch_multi([k64, k32], d_pay, d_off)
+        M = 1000
+        bk = torch.empty(len(lens), dtype=torch.int32, device=torch_dev)
+        rc = pmp.pmp_hash_batch_buckets(k64.handle, d_pay.data_ptr(), d_off.data_ptr(), len(lens), M, bk.data_ptr(),
+                                        None, torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        torch.cuda.synchronize()
+        for name, o, w in (("64", s64, w64), ("32", s32, w32), ("dual64", m64, w64), ("dual32", m32, w32)):
+            got = pmp.as_u64(o)
+            bad = np.nonzero(got != w)[0]
+            assert bad.size == 0, (name, [(int(i), int(lens[i])) for i in bad[:8]])
+        assert np.array_equal(bk.cpu().numpy().view(np.uint32), (w64 % M).astype(np.uint32))
+    finally:
+        pmp.pmp_set_small_batch_max(prev[0])
+        pmp.pmp_set_huge_min(prev[1])
+        pmp.pmp_set_huge_cap(prev[2])
+
+
 @pytest.mark.parametrize("order", [(64, 32), (32, 64), (64, 64, 32), (32,)])
 @pytest.mark.usefixtures("batch_path")
 def test_multi_schedule_fused_pass(torch_dev, oracle_lib, order):

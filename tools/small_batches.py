@@ -1,6 +1,9 @@
-"""Small batches (n <= 4096 strings, the k_small latency route) across length
-classes, against the throughput route (k_short + k_wstring, forced with
-pmp_set_small_batch_max(0)); also checks every digest against the oracle.
+"""Batches across length classes: small ones (n <= 4096 strings) through the
+latency route (k_small) and the throughput route (k_short + k_wstring + k_huge,
+forced with pmp_set_small_batch_max(0)); larger ones with a few huge strings
+through the throughput route with and without k_huge (pmp_set_huge_cap(0):
+every long string one warp) and with a lower huge threshold.  Every digest is
+checked against the oracle.
 
 python tools/small_batches.py   -- prints one line per (n, length) case:
 device time per call (CUDA events over back-to-back calls) on each route.
@@ -17,10 +20,19 @@ import oracle  # noqa: E402
 import paper_1609_09840_b200 as pmp  # noqa: E402
 
 CASES = [(1000, "U[1,64]"), (4096, "U[8,64]"), (4096, "4096"), (4096, "65536"), (1024, "262144"),
-         (64, "1048576"), (8, "4194304")]
+         (64, "1048576"), (8, "4194304"), (100_000, "U[8,64]+8x4M"), (100_000, "U[8,64]+2x64M"),
+         (20_000, "U[1,1M]log")]
 
 
 def lengths(n, spec, rng):
+    if spec.endswith("log"):   # log-uniform like configs[4]
+        return np.clip(np.floor(2.0 ** (20 * rng.random(n))), 1, 1 << 20).astype(np.uint64)
+    if "+" in spec:            # short strings with a few huge ones at random places
+        base, extra = spec.split("+")
+        cnt, size = extra.split("x")
+        lens = lengths(n, base, rng)
+        lens[rng.choice(n, int(cnt), replace=False)] = int(size[:-1]) << 20
+        return lens
     if spec.startswith("U["):
         lo, hi = (int(x) for x in spec[2:-1].split(","))
         return rng.integers(lo, hi + 1, size=n).astype(np.uint64)
@@ -41,7 +53,13 @@ def main():
         d_off = torch.from_numpy(offs.view(np.int64)).to(dev)
         want = oracle.hash_batch(okey, pay, offs, nthreads=os.cpu_count() or 4)
         row = []
-        for route, smax in (("small", default_max), ("throughput", 0)):
+        routes = [("small", default_max, 65536, 4 << 20), ("throughput", 0, 65536, 4 << 20)]
+        if n > default_max:
+            routes = [("throughput", 0, 65536, 4 << 20), ("no-huge", 0, 0, 4 << 20),
+                      ("huge>=256K", 0, 65536, 256 << 10)]
+        for route, smax, cap, hmin in routes:
+            prev_cap = pmp.pmp_set_huge_cap(cap)
+            prev_min = pmp.pmp_set_huge_min(hmin)
             pmp.pmp_set_small_batch_max(smax)
             out = torch.empty(n, dtype=torch.int64, device=dev)
             for _ in range(3):
@@ -57,7 +75,9 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             row.append(f"{route} {e0.elapsed_time(e1) / steps * 1e3:9.1f} us ({bad} mismatches)")
-        print(f"n={n:5d} len {spec:>8s} ({int(offs[-1]) / 2**20:8.1f} MiB): " + "  ".join(row), flush=True)
+            pmp.pmp_set_huge_cap(prev_cap)
+            pmp.pmp_set_huge_min(prev_min)
+        print(f"n={n:6d} len {spec:>13s} ({int(offs[-1]) / 2**20:8.1f} MiB): " + "  ".join(row), flush=True)
     pmp.pmp_set_small_batch_max(default_max)
 
 
