@@ -233,6 +233,51 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   }
 }
 
+#ifndef PMP_SHORT_APPEND_NOINLINE
+#define PMP_SHORT_APPEND_NOINLINE 0
+#endif
+// Long strings of a warp's 32 to the work lists (k_wstring's mid / big lists,
+// k_huge's list); out of line in tuning builds (PMP_SHORT_APPEND_NOINLINE)
+template <int BITS, bool DUAL>
+#if PMP_SHORT_APPEND_NOINLINE
+__device__ __noinline__
+#else
+PMP_DI
+#endif
+void append_long(const ParamKeys &K, uint32_t *__restrict__ wlist, uint32_t *__restrict__ wcount, uint64_t n,
+                 uint64_t i, uint64_t Bl, bool is_long, int lane) {
+  const unsigned lt = (1u << lane) - 1;
+  // huge strings (>= K.huge_min bytes) to the huge list (k_huge) while it
+  // has room (pmp_huge.cuh); the others: warp-aggregated append, big
+  // strings from the back, others from the front
+  const bool huge = is_long && Bl >= K.huge_min;
+  const unsigned hugemask = __ballot_sync(FULL, huge);
+  bool listed = is_long;
+  if (hugemask) {
+    uint32_t hbase = 0;
+    if (lane == 0) hbase = atomicAdd(&wcount[8], (uint32_t)__popc(hugemask));
+    hbase = __shfl_sync(FULL, hbase, 0);
+    const uint32_t slot = hbase + __popc(hugemask & lt);
+    if (huge && slot < K.huge_cap) {
+      uint32_t np = (uint32_t)huge_parts_of<BITS>(Bl);
+      if constexpr (DUAL) np = max(np, (uint32_t)huge_parts_of<32>(Bl));
+      huge_append(wlist, n, K.huge_cap, slot, (uint32_t)i, np);
+      listed = false;
+    }
+  }
+  const bool big = listed && Bl >= kBigBytes;
+  const unsigned bigmask = __ballot_sync(FULL, big), midmask = __ballot_sync(FULL, listed) & ~bigmask;
+  uint32_t mbase = 0, bbase = 0;
+  if (lane == 0) {
+    if (midmask) mbase = atomicAdd(&wcount[0], (uint32_t)__popc(midmask));
+    if (bigmask) bbase = atomicAdd(&wcount[1], (uint32_t)__popc(bigmask));
+  }
+  mbase = __shfl_sync(FULL, mbase, 0);
+  bbase = __shfl_sync(FULL, bbase, 0);
+  if (listed && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
+  if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
+}
+
 // k_short: warp-specialised TMA pipeline.  A block = 1 producer warp + kShortWarps
 // consumer warps, working on tiles of kTile = 32 * kShortWarps consecutive
 // strings (claimed dynamically, see below).  Shared memory holds
@@ -499,38 +544,7 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
     const bool is_long = !is_short;
     uint32_t B = (uint32_t)Bl;
     const unsigned longmask = __ballot_sync(FULL, is_long);
-    if (longmask) {
-      const unsigned lt = (1u << lane) - 1;
-      // huge strings (>= K.huge_min bytes) to the huge list (huge_pool) while it
-      // has room (pmp_huge.cuh); the others: warp-aggregated append, big
-      // strings from the back, others from the front
-      const bool huge = is_long && Bl >= K.huge_min;
-      const unsigned hugemask = __ballot_sync(FULL, huge);
-      bool listed = is_long;
-      if (hugemask) {
-        uint32_t hbase = 0;
-        if (lane == 0) hbase = atomicAdd(&wcount[8], (uint32_t)__popc(hugemask));
-        hbase = __shfl_sync(FULL, hbase, 0);
-        const uint32_t slot = hbase + __popc(hugemask & lt);
-        if (huge && slot < K.huge_cap) {
-          uint32_t np = (uint32_t)huge_parts_of<BITS>(Bl);
-          if constexpr (DUAL) np = max(np, (uint32_t)huge_parts_of<32>(Bl));
-          huge_append(wlist, n, K.huge_cap, slot, (uint32_t)i, np);
-          listed = false;
-        }
-      }
-      const bool big = listed && Bl >= kBigBytes;
-      const unsigned bigmask = __ballot_sync(FULL, big), midmask = __ballot_sync(FULL, listed) & ~bigmask;
-      uint32_t mbase = 0, bbase = 0;
-      if (lane == 0) {
-        if (midmask) mbase = atomicAdd(&wcount[0], (uint32_t)__popc(midmask));
-        if (bigmask) bbase = atomicAdd(&wcount[1], (uint32_t)__popc(bigmask));
-      }
-      mbase = __shfl_sync(FULL, mbase, 0);
-      bbase = __shfl_sync(FULL, bbase, 0);
-      if (listed && !big) wlist[mbase + __popc(midmask & lt)] = (uint32_t)i;
-      if (big) wlist[n - 1 - (bbase + __popc(bigmask & lt))] = (uint32_t)i;
-    }
+    if (longmask) append_long<BITS, DUAL>(K, wlist, wcount, n, i, Bl, is_long, lane);
     // warp max of the number of full words (the marker word is handled apart)
 #if PMP_SHORT_DIAG >= 3 && PMP_SHORT_DIAG <= 5  // diagnostic builds: the word loop capped at 4 words (what padding costs); 5: no loop
     const int tfm = min(PMP_SHORT_DIAG == 5 ? 0 : 4, (int)__reduce_max_sync(FULL, is_short ? B / (BITS / 8) : 0u));
