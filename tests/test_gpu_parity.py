@@ -29,17 +29,21 @@ def torch_dev():
     return torch.device("cuda:0")
 
 
-@pytest.fixture(params=["tensor", "wordloop", "latency"])
+@pytest.fixture(params=["tensor", "wordloop", "latency", "huge"])
 def batch_path(request, torch_dev):
     """Run a batch test through the throughput path with short strings on the
     tensor cores (k_short_tc + k_wstring), with short strings in the word loop
-    (k_short + k_wstring), and through the latency path (k_small, batches of
-    <= 4096 strings)."""
+    (k_short + k_wstring), through the latency path (k_small, batches of
+    <= 4096 strings), and through the word-loop throughput path with the huge
+    threshold lowered to 64 KiB (every string of >= 64 KiB node-parallel in
+    k_huge)."""
     prev = pmp.pmp_set_small_batch_max(4096 if request.param == "latency" else 0)
     prev_tc = pmp.pmp_set_short_tc(1 if request.param == "tensor" else 0)
+    prev_huge = pmp.pmp_set_huge_min(64 << 10 if request.param == "huge" else 4 << 20)
     yield request.param
     pmp.pmp_set_small_batch_max(prev)
     pmp.pmp_set_short_tc(prev_tc)
+    pmp.pmp_set_huge_min(prev_huge)
 
 
 def _u(bits):
