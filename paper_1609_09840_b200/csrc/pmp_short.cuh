@@ -9,6 +9,14 @@ namespace pmp {
 #ifndef PMP_SHORT_ORDER
 #define PMP_SHORT_ORDER 0
 #endif
+#ifndef PMP_SHORT_G0
+// the fused two-width loop runs its first G0 words without an exit test, then
+// tests every word (0: a test every PMP_SHORT_GD words).  configs[1] (warp
+// maximum 7 or 8 full words): G0 = 6 0.2462 ms, 7 0.2489, 5 0.2503, 4 0.2547,
+// 3 0.2582, 1 0.2665, against 0.2508 for a test every 8 words
+// (profiles/r02/s_loop_g0.txt)
+#define PMP_SHORT_G0 6
+#endif
 #ifndef PMP_SHORT_BRANCHLESS
 #define PMP_SHORT_BRANCHLESS 1   // marker-word branches as selects: configs[1] 0.2691 -> 0.2652 ms
 #endif
@@ -132,10 +140,10 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   macc_zero(A);
   Acc3 C = {0, 0, 0};
   uint32_t y0 = fetch(0);
-  // exit test granularity (PMP_SHORT_GD): the warp maximum is 7 or 8 full words
-  // for configs[1]; every 8 words measured 0.4% faster than every 4 on the
-  // final round-2 code (stable to 0.1% with the bench's head start), 5% faster
-  // than every 2 (profiles/r02/s_knobs_final.txt)
+  // exit test granularity (PMP_SHORT_GD, when PMP_SHORT_G0 is 0): the warp
+  // maximum is 7 or 8 full words for configs[1]; every 8 words measured 0.4%
+  // faster than every 4 on the round-2 code (stable to 0.1% with the bench's
+  // head start), 5% faster than every 2 (profiles/r02/s_knobs_final.txt)
 #if PMP_SHORT_DIAG >= 3 && PMP_SHORT_DIAG <= 5   // (diagnostic builds 3-5: the loop capped, see below)
   constexpr int G = 4;
 #else
@@ -144,6 +152,41 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
 #endif
   constexpr int G = V2 ? kShortG64 : PMP_SHORT_GD;
 #endif
+  auto step = [&](int t) {                                   // full 64-bit word t (both widths)
+    const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
+    const uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
+    y0 = y2;
+    // both halves of a full 64-bit word are full PM+32 words; the one PM+32
+    // word beyond them (the low half at t = tl64 when B mod 8 >= 4) is added
+    // with the markers below
+    const bool f64 = t < tl64;
+    const uint32_t lm = f64 ? lo : 0u, hm = f64 ? hi : 0u;
+    if (t < 15) {
+#if PMP_SHORT_ORDER   // (tuning build: the PM+32 multiply-adds first)
+      mac32(C, K.a32[2 * t], lm);
+      mac32(C, K.a32[2 * t + 1], hm);
+      mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lm, hm);
+#else
+#if PMP_SHORT_DIAG != 7   // (diagnostic builds 6 / 7: one width's loop multiply-adds left out)
+      mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lm, hm);  // Eq. (1)
+#endif
+#if PMP_SHORT_DIAG != 6
+      mac32(C, K.a32[2 * t], lm);
+      mac32(C, K.a32[2 * t + 1], hm);
+#endif
+#endif
+    }
+  };
+#if PMP_SHORT_G0 && !(PMP_SHORT_DIAG >= 3 && PMP_SHORT_DIAG <= 5)
+  // the first PMP_SHORT_G0 words without exit tests, then a test per word
+  if (V2 || tfull_max > 0) {
+#pragma unroll
+    for (int t = 0; t < 15; t++) {
+      if (t >= PMP_SHORT_G0 && t >= tfull_max) break;      // warp-uniform
+      step(t);
+    }
+  }
+#else
 #pragma unroll
   for (int tb = 0; tb < 16; tb += G) {
     if (tb >= tfull_max) break;                              // warp-uniform
@@ -151,31 +194,10 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
     for (int j = 0; j < G; j++) {
       const int t = tb + j;
       if (t >= 16) break;                                    // compile-time
-      const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
-      const uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
-      y0 = y2;
-      // both halves of a full 64-bit word are full PM+32 words; the one PM+32
-      // word beyond them (the low half at t = tl64 when B mod 8 >= 4) is added
-      // with the markers below
-      const bool f64 = t < tl64;
-      const uint32_t lm = f64 ? lo : 0u, hm = f64 ? hi : 0u;
-      if (t < 15) {
-#if PMP_SHORT_ORDER   // (tuning build: the PM+32 multiply-adds first)
-        mac32(C, K.a32[2 * t], lm);
-        mac32(C, K.a32[2 * t + 1], hm);
-        mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lm, hm);
-#else
-#if PMP_SHORT_DIAG != 7   // (diagnostic builds 6 / 7: one width's loop multiply-adds left out)
-        mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lm, hm);  // Eq. (1)
-#endif
-#if PMP_SHORT_DIAG != 6
-        mac32(C, K.a32[2 * t], lm);
-        mac32(C, K.a32[2 * t + 1], hm);
-#endif
-#endif
-      }
+      step(t);
     }
   }
+#endif
   // marker words: the 8 bytes at 8 tl64, and its half holding byte 4 tl32
   const uint32_t z0 = fetch(2 * tl64), z1 = fetch(2 * tl64 + 1), z2 = fetch(2 * tl64 + 2);
   const uint32_t zl = funnel(z0, z1, sh), zh = funnel(z1, z2, sh);
