@@ -17,6 +17,9 @@ namespace pmp {
 // (profiles/r02/s_loop_g0.txt)
 #define PMP_SHORT_G0 6
 #endif
+#ifndef PMP_SHORT_G1
+#define PMP_SHORT_G1 1   // after the first G0 words, an exit test every G1 words
+#endif
 #ifndef PMP_SHORT_BRANCHLESS
 #define PMP_SHORT_BRANCHLESS 1   // marker-word branches as selects: configs[1] 0.2691 -> 0.2652 ms
 #endif
@@ -182,7 +185,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   if (V2 || tfull_max > 0) {
 #pragma unroll
     for (int t = 0; t < 15; t++) {
-      if (t >= PMP_SHORT_G0 && t >= tfull_max) break;      // warp-uniform
+      if (t >= PMP_SHORT_G0 && (t - PMP_SHORT_G0) % PMP_SHORT_G1 == 0 && t >= tfull_max) break;  // warp-uniform
       step(t);
     }
   }
