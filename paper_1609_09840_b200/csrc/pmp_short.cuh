@@ -17,6 +17,9 @@ namespace pmp {
 // (profiles/r02/s_loop_g0.txt)
 #define PMP_SHORT_G0 6
 #endif
+#ifndef PMP_SHORT_MARKER_EARLY
+#define PMP_SHORT_MARKER_EARLY 0
+#endif
 #ifndef PMP_SHORT_G1
 #define PMP_SHORT_G1 1   // after the first G0 words, an exit test every G1 words
 #endif
@@ -142,6 +145,9 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   MacAcc64 A;
   macc_zero(A);
   Acc3 C = {0, 0, 0};
+#if PMP_SHORT_MARKER_EARLY   // (tuning: the marker words' loads issued before the loop)
+  const uint32_t z0 = fetch(2 * tl64), z1 = fetch(2 * tl64 + 1), z2 = fetch(2 * tl64 + 2);
+#endif
   uint32_t y0 = fetch(0);
   // exit test granularity (PMP_SHORT_GD, when PMP_SHORT_G0 is 0): the warp
   // maximum is 7 or 8 full words for configs[1]; every 8 words measured 0.4%
@@ -202,7 +208,9 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   }
 #endif
   // marker words: the 8 bytes at 8 tl64, and its half holding byte 4 tl32
+#if !PMP_SHORT_MARKER_EARLY
   const uint32_t z0 = fetch(2 * tl64), z1 = fetch(2 * tl64 + 1), z2 = fetch(2 * tl64 + 2);
+#endif
   const uint32_t zl = funnel(z0, z1, sh), zh = funnel(z1, z2, sh);
   // the partial 32-bit word is the PM+32 marker word, and a half of the PM+64 one
   const bool up = (B & 4) != 0;                              // B mod 8 >= 4
