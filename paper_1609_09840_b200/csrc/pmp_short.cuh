@@ -17,6 +17,9 @@ namespace pmp {
 // (profiles/r02/s_loop_g0.txt)
 #define PMP_SHORT_G0 6
 #endif
+#ifndef PMP_SHORT_PF
+#define PMP_SHORT_PF 0
+#endif
 #ifndef PMP_SHORT_MARKER_EARLY
 #define PMP_SHORT_MARKER_EARLY 0
 #endif
@@ -154,15 +157,14 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   // faster than every 4 on the round-2 code (stable to 0.1% with the bench's
   // head start), 5% faster than every 2 (profiles/r02/s_knobs_final.txt)
 #if PMP_SHORT_DIAG >= 3 && PMP_SHORT_DIAG <= 5   // (diagnostic builds 3-5: the loop capped, see below)
-  constexpr int G = 4;
+  [[maybe_unused]] constexpr int G = 4;
 #else
 #ifndef PMP_SHORT_GD
 #define PMP_SHORT_GD 8   // exit test every 8 words (final round-2 code: 0.2649 vs 0.2660 ms for 4, 0.2787 for 2)
 #endif
-  constexpr int G = V2 ? kShortG64 : PMP_SHORT_GD;
+  [[maybe_unused]] constexpr int G = V2 ? kShortG64 : PMP_SHORT_GD;   // (the PMP_SHORT_G0 == 0 loop)
 #endif
-  auto step = [&](int t) {                                   // full 64-bit word t (both widths)
-    const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
+  auto step2 = [&](int t, uint32_t y1, uint32_t y2) {       // full 64-bit word t (both widths)
     const uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
     y0 = y2;
     // both halves of a full 64-bit word are full PM+32 words; the one PM+32
@@ -186,14 +188,31 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
 #endif
     }
   };
+  auto step = [&](int t) { step2(t, fetch(2 * t + 1), fetch(2 * t + 2)); };
 #if PMP_SHORT_G0 && !(PMP_SHORT_DIAG >= 3 && PMP_SHORT_DIAG <= 5)
   // the first PMP_SHORT_G0 words without exit tests, then a test per word
   if (V2 || tfull_max > 0) {
+#if PMP_SHORT_PF   // (tuning: the tested words' loads issued one word ahead, before each test)
+#pragma unroll
+    for (int t = 0; t < PMP_SHORT_G0; t++) step(t);
+    uint32_t n1 = fetch(2 * PMP_SHORT_G0 + 1), n2 = fetch(2 * PMP_SHORT_G0 + 2);
+#pragma unroll
+    for (int t = PMP_SHORT_G0; t < 15; t++) {
+      if (t >= tfull_max) break;                             // warp-uniform
+      const uint32_t y1 = n1, y2 = n2;
+      if (t + 1 < 15) {
+        n1 = fetch(2 * t + 3);
+        n2 = fetch(2 * t + 4);
+      }
+      step2(t, y1, y2);
+    }
+#else
 #pragma unroll
     for (int t = 0; t < 15; t++) {
       if (t >= PMP_SHORT_G0 && (t - PMP_SHORT_G0) % PMP_SHORT_G1 == 0 && t >= tfull_max) break;  // warp-uniform
       step(t);
     }
+#endif
   }
 #else
 #pragma unroll
