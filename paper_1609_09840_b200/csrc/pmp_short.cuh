@@ -17,6 +17,9 @@ namespace pmp {
 // (profiles/r02/s_loop_g0.txt)
 #define PMP_SHORT_G0 6
 #endif
+#ifndef PMP_SHORT_FIN32_FIRST
+#define PMP_SHORT_FIN32_FIRST 0
+#endif
 #ifndef PMP_SHORT_PF
 #define PMP_SHORT_PF 0
 #endif
@@ -238,6 +241,19 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
   const uint64_t w = up ? ((uint64_t)w32 << 32) | zl : (uint64_t)w32;
 #if PMP_SHORT_BRANCHLESS   // the marker-word branches as selects (tree pass)
   if constexpr (!V2) {
+#if PMP_SHORT_FIN32_FIRST   // (tuning: the PM+32 finish first)
+    mac32(C, up ? skeys32[2 * tl64] : 0u, zl);
+    mac32(C, skeys32[tl32], w32);
+    acc3_add_u64(C, K.b32);
+    const uint32_t r32 = reduce_lo_acc3(C);
+    lo32 = tl32 == 0 ? w32 : r32;
+    mac64(A, skeys[tl64], w);
+    Acc5 x = macc_normalize(A);
+    acc5_add_u64(x, K.b);
+    const uint64_t r64 = reduce_lo_acc5(x);
+    lo64 = tl64 == 0 ? w : r64;
+    return;
+#else
     mac32(C, up ? skeys32[2 * tl64] : 0u, zl);               // the full PM+32 word 2 tl64 (key 0 if none)
     mac64(A, skeys[tl64], w);
     Acc5 x = macc_normalize(A);
@@ -249,6 +265,7 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
     const uint32_t r32 = reduce_lo_acc3(C);
     lo32 = tl32 == 0 ? w32 : r32;
     return;
+#endif
   }
 #endif
   if (up) mac32(C, skeys32[2 * tl64], zl);                   // the full PM+32 word 2 tl64 (a select here: +0.3% slower)

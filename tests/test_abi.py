@@ -208,3 +208,19 @@ def test_two_level_variant_arguments(L):
     if not torch.cuda.is_available():
         assert pmp.pmp_hash2_long(k.handle, 8, 10, 8, 0) == pmp.PMP_ENODEV
         assert pmp.pmp_hash2_batch(k.handle, 8, 8, 1, 8, 0) == pmp.PMP_ENODEV
+
+
+def test_routing_hooks_set_and_query(L):
+    """Batch-routing hooks are host state: each returns the previous value;
+    pmp_set_huge_min(0) only queries (include/pmp.h)."""
+    prev_min = pmp.pmp_set_huge_min(0)
+    assert prev_min == 4 << 20                       # the documented default
+    assert pmp.pmp_set_huge_min(1 << 20) == prev_min
+    assert pmp.pmp_set_huge_min(0) == 1 << 20
+    assert pmp.pmp_set_huge_min(prev_min) == 1 << 20
+    prev_cap = pmp.pmp_set_huge_cap(7)
+    assert prev_cap == 65536
+    assert pmp.pmp_set_huge_cap(prev_cap) == 7
+    prev_small = pmp.pmp_set_small_batch_max(100)
+    assert prev_small == 4096
+    assert pmp.pmp_set_small_batch_max(prev_small) == 100
