@@ -17,6 +17,12 @@ namespace pmp {
 // (profiles/r02/s_loop_g0.txt)
 #define PMP_SHORT_G0 6
 #endif
+#ifndef PMP_SHORT_ANDMASK
+#define PMP_SHORT_ANDMASK 0
+#endif
+#ifndef PMP_SHORT_NESTED
+#define PMP_SHORT_NESTED 0
+#endif
 #ifndef PMP_SHORT_FIN32_FIRST
 #define PMP_SHORT_FIN32_FIRST 0
 #endif
@@ -174,7 +180,12 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
     // word beyond them (the low half at t = tl64 when B mod 8 >= 4) is added
     // with the markers below
     const bool f64 = t < tl64;
+#if PMP_SHORT_ANDMASK   // (tuning: the masks as AND with an all-ones / zero word)
+    const uint32_t msk = 0u - (uint32_t)f64;
+    const uint32_t lm = lo & msk, hm = hi & msk;
+#else
     const uint32_t lm = f64 ? lo : 0u, hm = f64 ? hi : 0u;
+#endif
     if (t < 15) {
 #if PMP_SHORT_ORDER   // (tuning build: the PM+32 multiply-adds first)
       mac32(C, K.a32[2 * t], lm);
@@ -208,6 +219,20 @@ PMP_DI void short_tree_dual(const ParamKeys &K, const uint64_t *__restrict__ ske
         n2 = fetch(2 * t + 4);
       }
       step2(t, y1, y2);
+    }
+#elif PMP_SHORT_NESTED   // (tuning: the tested words as nested ifs, t = G0, G0 + 1 only, then the loop)
+#pragma unroll
+    for (int t = 0; t < PMP_SHORT_G0; t++) step(t);
+    if (tfull_max > PMP_SHORT_G0) {
+      step(PMP_SHORT_G0);
+      if (tfull_max > PMP_SHORT_G0 + 1) {
+        step(PMP_SHORT_G0 + 1);
+#pragma unroll
+        for (int t = PMP_SHORT_G0 + 2; t < 15; t++) {
+          if (t >= tfull_max) break;
+          step(t);
+        }
+      }
     }
 #else
 #pragma unroll
