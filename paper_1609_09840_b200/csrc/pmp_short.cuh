@@ -17,6 +17,9 @@ namespace pmp {
 // (profiles/r02/s_loop_g0.txt)
 #define PMP_SHORT_G0 6
 #endif
+#ifndef PMP_SHORT_STATIC_FIRST
+#define PMP_SHORT_STATIC_FIRST 0
+#endif
 #ifndef PMP_SHORT_ANDMASK
 #define PMP_SHORT_ANDMASK 0
 #endif
@@ -507,18 +510,22 @@ k_short(const ParamKeys K, const uint8_t *__restrict__ bytes, const uint64_t *__
 #else
     constexpr bool kClaimAhead = !DUAL;
 #endif
+    // (PMP_SHORT_STATIC_FIRST: block b's first tile is tile b, claimed
+    // without an atomic; later claims draw from the counter + gridDim.x)
+    const uint32_t cbase = PMP_SHORT_STATIC_FIRST ? gridDim.x : 0u;
     uint32_t claim = 0;
-    if (kClaimAhead && lane == 0) claim = atomicAdd(tile_ctr, 1u);
+    if (kClaimAhead && lane == 0) claim = PMP_SHORT_STATIC_FIRST ? blockIdx.x : atomicAdd(tile_ctr, 1u);
     auto issue_offs = [&](uint32_t k) {
       if (k >= kRing) wait_done(k - kRing);  // slot reuse
-      if (!kClaimAhead && lane == 0) claim = atomicAdd(tile_ctr, 1u);
+      if (!kClaimAhead && lane == 0)
+        claim = (PMP_SHORT_STATIC_FIRST && k == 0) ? blockIdx.x : cbase + atomicAdd(tile_ctr, 1u);
       const uint32_t t = __shfl_sync(FULL, claim, 0);
       if (t >= ntiles) {
         k_end = k;
         return;
       }
       if (lane == 0) {
-        if (kClaimAhead) claim = atomicAdd(tile_ctr, 1u);  // for the next call
+        if (kClaimAhead) claim = cbase + atomicAdd(tile_ctr, 1u);  // for the next call
         const int q = (int)(k & (kRing - 1));
         tids[q] = t;
         const uint64_t base = (uint64_t)t * kTile;
