@@ -17,6 +17,17 @@ namespace pmp {
 // (profiles/r02/s_loop_g0.txt)
 #define PMP_SHORT_G0 6
 #endif
+#ifndef PMP_SHORT_G0_64
+// single-width loops (bucket mode, --separate-widths, the two-level variant's
+// single schedule, k_small): the first G0 words untested, then a test per word
+// (0: a test every kShortG64 / kShortG32 words).  configs[1] separate widths:
+// 0.3859 -> 0.3822 ms with 6 / 13 (5 / 12: 0.3816-0.3822, 7 / 14: 0.3851;
+// profiles/r02/s_loop_g0.txt)
+#define PMP_SHORT_G0_64 6
+#endif
+#ifndef PMP_SHORT_G0_32
+#define PMP_SHORT_G0_32 13
+#endif
 #ifndef PMP_SHORT_STATIC_FIRST
 #define PMP_SHORT_STATIC_FIRST 0
 #endif
@@ -62,6 +73,22 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
     MacAcc64 A;
     macc_zero(A);
     uint32_t y0 = fetch(0);
+    auto step = [&](int t, uint32_t y1, uint32_t y2) {
+      uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
+      y0 = y2;
+      if ((uint32_t)t >= (uint32_t)tlast) lo = hi = 0;         // past this lane's full words
+      mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lo, hi);  // Eq. (1), lazy
+    };
+#if PMP_SHORT_G0_64
+    // the first PMP_SHORT_G0_64 words without exit tests, then a test per word
+    if (V2 || tfull_max > 0) {
+#pragma unroll
+      for (int t = 0; t < 15; t++) {
+        if (t >= PMP_SHORT_G0_64 && t >= tfull_max) break;    // warp-uniform
+        step(t, fetch(2 * t + 1), fetch(2 * t + 2));
+      }
+    }
+#else
 #pragma unroll
     for (int tb = 0; tb < 16; tb += kShortG64) {
       if (tb >= tfull_max) break;                              // warp-uniform, once per kShortG64 words
@@ -69,13 +96,10 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
       for (int j = 0; j < kShortG64; j++) {
         const int t = tb + j;
         if (t >= 15) break;                                    // compile-time
-        const uint32_t y1 = fetch(2 * t + 1), y2 = fetch(2 * t + 2);
-        uint32_t lo = funnel(y0, y1, sh), hi = funnel(y1, y2, sh);
-        y0 = y2;
-        if ((uint32_t)t >= (uint32_t)tlast) lo = hi = 0;       // past this lane's full words
-        mac64(A, (uint32_t)K.a[t], (uint32_t)(K.a[t] >> 32), lo, hi);  // Eq. (1), lazy
+        step(t, fetch(2 * t + 1), fetch(2 * t + 2));
       }
     }
+#endif
     const uint32_t z0 = fetch(2 * tlast), z1 = fetch(2 * tlast + 1), z2 = fetch(2 * tlast + 2);
     const uint32_t zl = funnel(z0, z1, sh), zh = funnel(z1, z2, sh);
     // bytes || 0x01 || 0: mask the half holding byte r, keep / drop the other
@@ -107,6 +131,22 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
     const uint32_t r = B & 3;
     Acc3 A = {0, 0, 0};
     uint32_t y0 = fetch(0);
+    auto step = [&](int t, uint32_t y1) {
+      uint32_t w = funnel(y0, y1, sh);
+      y0 = y1;
+      if ((uint32_t)t >= (uint32_t)tlast) w = 0;
+      mac32(A, (uint32_t)K.a[t], w);
+    };
+#if PMP_SHORT_G0_32
+    // the first PMP_SHORT_G0_32 words without exit tests, then a test per word
+    if (V2 || tfull_max > 0) {
+#pragma unroll
+      for (int t = 0; t < 31; t++) {
+        if (t >= PMP_SHORT_G0_32 && t >= tfull_max) break;    // warp-uniform
+        step(t, fetch(t + 1));
+      }
+    }
+#else
 #pragma unroll
     for (int tb = 0; tb < 32; tb += kShortG32) {
       if (tb >= tfull_max) break;                              // warp-uniform, once per kShortG32 words
@@ -114,13 +154,10 @@ PMP_DI uint64_t short_tree_lo(const ParamKeys &K, const uint64_t *__restrict__ s
       for (int j = 0; j < kShortG32; j++) {
         const int t = tb + j;
         if (t >= 31) break;
-        const uint32_t y1 = fetch(t + 1);
-        uint32_t w = funnel(y0, y1, sh);
-        y0 = y1;
-        if ((uint32_t)t >= (uint32_t)tlast) w = 0;
-        mac32(A, (uint32_t)K.a[t], w);
+        step(t, fetch(t + 1));
       }
     }
+#endif
     const uint32_t z0 = fetch(tlast), z1 = fetch(tlast + 1);
     uint32_t w = funnel(z0, z1, sh);
     w = (w & ((1u << (8 * r)) - 1)) | (1u << (8 * r));
