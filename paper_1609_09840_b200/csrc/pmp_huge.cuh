@@ -86,11 +86,17 @@ PMP_DI void huge_pool(const uint64_t *__restrict__ keys, const uint8_t *__restri
     if (lane == 0) x = atomicAdd(cursor, 1ull);
     x = __shfl_sync(FULL, x, 0);
     if (x >= total) break;
-    uint32_t lo = 0, hi = nh - 1;                      // the last slot whose first part <= x
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi + 1) >> 1;
-      if (__ldcg(hst + (size_t)kHugeState * mid + 5) <= x) lo = mid;
-      else hi = mid - 1;
+    // the last slot whose first part <= x: a 32-way search (one load per lane
+    // and round, ~log32(nh) dependent rounds instead of log2(nh)); invariant
+    // first[lo] <= x < first[hi] (hi == nh: no bound)
+    uint32_t lo = 0, hi = nh;
+    while (hi - lo > 1) {
+      const uint32_t step = (hi - lo + 31) / 32;
+      const uint32_t h = lo + (uint32_t)lane * step;
+      const bool le = h < hi && __ldcg(hst + (size_t)kHugeState * h + 5) <= x;
+      const int k = 31 - __clz(__ballot_sync(FULL, le));   // lane 0 always (h = lo)
+      lo += (uint32_t)k * step;
+      hi = min(hi, lo + step);
     }
     uint64_t *st = hst + (size_t)kHugeState * lo;
     const uint64_t p = x - __ldcg(st + 5), np = st[4] >> 32;
